@@ -1,0 +1,131 @@
+/* edaa_b200.h — the C-ABI of the B200-native EDAA hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, status codes, no
+ * exceptions and no CUDA/torch types in the signatures.  The C++ drop-in
+ * layer (include/archetype/*.hpp, implemented in
+ * paper_2209_11002_b200/csrc/host/) and the Python surface
+ * (paper_2209_11002_b200/edaa.py) are both thin callers of it.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj):
+ *   edaa_set_image*    the X argument of run()/run_ensemble()
+ *                      (solver.hpp:81, ensemble.hpp:68-69; HsiImage image.hpp:18-28)
+ *   edaa_solve*        run() — Algorithm 1 (solver.cpp:190-238) for a BATCH of
+ *                      runs (seeds/gammas per run, ensemble.cpp:117-139)
+ *   edaa_run_record    RunRecord / RunResult scalars (ensemble.hpp:31-40,
+ *                      solver.hpp:29-38) incl. the archetype::Error message of a
+ *                      failed run (ensemble.cpp:133-136)
+ *   edaa_traces        RunResult::objective_trace (solver.hpp:37)
+ *   edaa_factors       RunResult::{abundances, contributions, endmembers}
+ *   edaa_select        select_runs() (ensemble.hpp:63, ensemble.cpp:71-94)
+ *   edaa_solve_observed the StepObserver hook (solver.hpp:69-77,81)
+ *
+ * Threading: one context per device; a context is not thread-safe (the
+ * C++ layer serialises).  All device memory is owned by the context.
+ *
+ * Precision contract: X is stored as fp32 (callers round once); every
+ * contraction with X, every per-pixel update and every reduction is fp64.
+ */
+#ifndef EDAA_B200_H
+#define EDAA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define EDAA_API __attribute__((visibility("default")))
+#else
+#define EDAA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct edaa_ctx edaa_ctx;
+
+enum {
+  EDAA_OK = 0,
+  EDAA_ERR_INVALID = 1,     /* bad argument */
+  EDAA_ERR_CUDA = 2,        /* CUDA runtime failure (message in edaa_last_error) */
+  EDAA_ERR_UNSUPPORTED = 3, /* shape outside the compiled kernels (p > 16, L > 320) */
+  EDAA_ERR_STATE = 4,       /* call out of order (no image / no solve) */
+  EDAA_ERR_ALL_FAILED = 5   /* edaa_select: "every run failed" (ensemble.cpp:79-80) */
+};
+
+/* Per-run failure codes (RunRecord.ok == false), see edaa_run_record. */
+enum {
+  EDAA_RUN_OK = 0,
+  EDAA_RUN_NONFINITE_A = 1,    /* solver.cpp:72-75 on the abundance block */
+  EDAA_RUN_NONFINITE_B = 2,    /* solver.cpp:72-75 on the contribution block */
+  EDAA_RUN_DEGENERATE = 3,     /* solver.cpp:141 */
+  EDAA_RUN_SPECTRAL_BAD = 4,   /* matrix.cpp:151-152 */
+  EDAA_RUN_SPECTRAL_NOCONV = 5 /* matrix.cpp:186-189 */
+};
+
+typedef struct {
+  size_t endmembers;     /* p  (SolverConfig::endmembers, solver.hpp:16) */
+  size_t outer_iters;    /* T  (solver.hpp:17) */
+  size_t inner_iters_a;  /* K1 (solver.hpp:18) */
+  size_t inner_iters_b;  /* K2 (solver.hpp:19) */
+  size_t runs;           /* M runs batched on this device */
+  const uint64_t* seeds; /* [runs] host: SolverConfig::seed of each run */
+  const double* gammas;  /* [runs] host: SolverConfig::gamma of each run */
+} edaa_solve_params;
+
+typedef struct {
+  double fit_l1;      /* RunResult::fit_l1 */
+  double coherence;   /* RunResult::coherence */
+  double eta_a;       /* StepSizes::eta_a (solver.hpp:48-51) */
+  double eta_b;
+  int ok;             /* 1 if the run finished (RunRecord::ok) */
+  int fail_code;      /* EDAA_RUN_* */
+  size_t fail_outer;  /* outer iteration named in the message (when applicable) */
+  char message[192];  /* the reference's archetype::Error text, "" when ok */
+} edaa_run_record;
+
+/* Context lifetime. device = CUDA ordinal. */
+EDAA_API int edaa_create(int device, edaa_ctx** out);
+EDAA_API int edaa_destroy(edaa_ctx* ctx);
+EDAA_API const char* edaa_last_error(const edaa_ctx* ctx);
+/* The cudaStream_t all work is enqueued on (as void*), for event timing. */
+EDAA_API void* edaa_stream(edaa_ctx* ctx);
+
+/* Image X (L×N row-major fp32, bands × pixels, already ℓ2-normalised and
+ * validated by the caller).  _host copies from host memory (pinned or
+ * pageable); _device copies from a device pointer with row pitch ld (floats). */
+EDAA_API int edaa_set_image_host(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels);
+EDAA_API int edaa_set_image_device(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels, size_t ld);
+
+/* Batched Algorithm 1 over all runs.  _async only enqueues on edaa_stream();
+ * edaa_finish waits and fetches the per-run records.  edaa_solve = both. */
+EDAA_API int edaa_solve_async(edaa_ctx* ctx, const edaa_solve_params* params);
+EDAA_API int edaa_finish(edaa_ctx* ctx);
+EDAA_API int edaa_solve(edaa_ctx* ctx, const edaa_solve_params* params);
+
+/* Results of the last solve. */
+EDAA_API int edaa_run_record_get(edaa_ctx* ctx, size_t run, edaa_run_record* out);
+EDAA_API int edaa_traces(edaa_ctx* ctx, double* out /* [runs][T+1] */);
+/* Any pointer may be NULL. a: p×N, b: N×p, e: L×p (reference layouts). */
+EDAA_API int edaa_factors(edaa_ctx* ctx, size_t run, double* a, double* b, double* e);
+/* Model selection on device over the last solve's records (ensemble.cpp:71-94).
+ * cand: [runs] bytes; returns EDAA_ERR_ALL_FAILED when no run is ok. */
+EDAA_API int edaa_select(edaa_ctx* ctx, double fit_slack, uint8_t* cand, size_t* selected,
+                double* fit_min);
+
+/* Observed mode (StepObserver): a single run (runs == 1) whose every inner
+ * iterate is delivered, in order, to the callback as host arrays
+ * (a: p×N, b: N×p).  block is 'A' or 'B'. */
+typedef void (*edaa_observer_fn)(size_t outer, char block, size_t inner, const double* a,
+                                 const double* b, size_t p, size_t n, void* user);
+EDAA_API int edaa_solve_observed(edaa_ctx* ctx, const edaa_solve_params* params, edaa_observer_fn fn,
+                        void* user);
+
+/* Version / capability probe. */
+EDAA_API const char* edaa_version(void);
+EDAA_API size_t edaa_max_endmembers(void);
+EDAA_API size_t edaa_max_bands(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EDAA_B200_H */

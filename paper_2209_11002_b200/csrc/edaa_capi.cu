@@ -1,0 +1,620 @@
+// C-ABI (include/edaa_b200.h): device context, buffer management and the
+// per-solve launch schedule of the batched EDAA solver.
+//
+// Launch schedule of one solve (M runs batched, all on one stream):
+//   init pass (B⁰ logits from SplitMix64, Y⁰ = X·B⁰)  → combine → post(init: G, η)
+//   for t = 1..T:
+//     A pass (trace[t-1], K1 steps, XAᵀ, AAᵀ)          → combine → post(Z)
+//     for k = 1..K2:
+//       B pass (g = XᵀZ, logits, online max, Y_{k+1})   → combine → post(Z or G)
+//   objective pass (trace[T]) → combine; materialise B; E = X·B (reference
+//   order); fit_l1; coherence.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/edaa_b200.h"
+#include "edaa_internal.cuh"
+
+using edaa::Dims;
+
+struct edaa_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // image
+  float* X = nullptr;
+  double* xnorm = nullptr;
+  int L = 0, N = 0, Npad = 0;
+  size_t x_cap = 0, xn_cap = 0;
+  // solve state
+  bool solved = false;
+  Dims d{};
+  size_t T = 0;
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  Buf A, Lg, Bv, Y, Z, XAt, AAt, Gbuf, colm, colS, collogS, eta_a, eta_b, gamma, trace, part_C,
+      part_m, part_S, part_obj, E, fit, mu, part_fit, seeds, fail_key, fail_code, fail_value, cand,
+      selected, fit_min, obsA;
+  int fit_blocks = 0;
+  // host copies of the per-run records
+  std::vector<double> h_fit, h_mu, h_eta_a, h_eta_b, h_fail_value, h_trace;
+  std::vector<int> h_fail_code;
+  std::vector<unsigned long long> h_fail_key;
+};
+
+namespace {
+
+int set_err(edaa_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(edaa_ctx* c, cudaError_t e, const char* what) {
+  return set_err(c, EDAA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define EDAA_CUDA(ctx, call)                                   \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #call); \
+  } while (0)
+
+cudaError_t ensure(edaa_ctx::Buf& b, size_t bytes) {
+  if (b.cap >= bytes && b.p) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  cudaError_t e = cudaMalloc(&b.p, std::max<size_t>(bytes, 16));
+  if (e == cudaSuccess) b.cap = std::max<size_t>(bytes, 16);
+  return e;
+}
+
+template <class T>
+T* P(edaa_ctx::Buf& b) {
+  return static_cast<T*>(b.p);
+}
+
+__global__ void k_fill_a(double* A, int M, int p, int N, int Npad) {
+  const size_t total = static_cast<size_t>(M) * p * Npad;
+  const double v = 1.0 / static_cast<double>(p);  // init_abundances, solver.cpp:113-116
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i % Npad);
+    A[i] = (j < N) ? v : 0.0;
+  }
+}
+
+__global__ void k_pad_copy(const float* src, size_t ld, float* dst, int L, int N, int Npad) {
+  const size_t total = static_cast<size_t>(L) * Npad;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int l = static_cast<int>(i / Npad), j = static_cast<int>(i % Npad);
+    dst[i] = (j < N) ? src[static_cast<size_t>(l) * ld + j] : 0.0f;
+  }
+}
+
+std::string run_message(int code, size_t outer, double value) {
+  char buf[192];
+  switch (code) {
+    case EDAA_RUN_NONFINITE_A:
+      std::snprintf(buf, sizeof buf, "non-finite abundance iterate at outer iteration %zu", outer);
+      return buf;
+    case EDAA_RUN_NONFINITE_B:
+      std::snprintf(buf, sizeof buf, "non-finite contribution iterate at outer iteration %zu", outer);
+      return buf;
+    case EDAA_RUN_DEGENERATE:
+      return "degenerate initialization: X\xc2\xb7" "B0 is zero";
+    case EDAA_RUN_SPECTRAL_BAD:
+      return "spectral_norm: matrix must be finite and nonzero";
+    case EDAA_RUN_SPECTRAL_NOCONV:
+      std::snprintf(buf, sizeof buf,
+                    "spectral_norm: no convergence after 1000 iterations; best estimate %g", value);
+      return buf;
+    default:
+      return "";
+  }
+}
+
+int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
+  if (!prm || !prm->seeds || !prm->gammas) return set_err(c, EDAA_ERR_INVALID, "null params");
+  if (c->X == nullptr) return set_err(c, EDAA_ERR_STATE, "no image set");
+  const size_t p = prm->endmembers;
+  if (p < 2) return set_err(c, EDAA_ERR_INVALID, "solver config: endmember count must be at least 2");
+  if (prm->outer_iters < 1 || prm->inner_iters_a < 1 || prm->inner_iters_b < 1)
+    return set_err(c, EDAA_ERR_INVALID, "solver config: iteration counts must be at least 1");
+  if (prm->runs < 1) return set_err(c, EDAA_ERR_INVALID, "ensemble needs at least one run");
+  if (p > static_cast<size_t>(edaa::kMaxP))
+    return set_err(c, EDAA_ERR_UNSUPPORTED, "endmember count above the compiled maximum (16)");
+  for (size_t r = 0; r < prm->runs; ++r)
+    if (!(prm->gammas[r] > 0.0) || !std::isfinite(prm->gammas[r]))
+      return set_err(c, EDAA_ERR_INVALID, "solver config: step factor gamma must be positive");
+  Dims d{};
+  d.L = c->L;
+  d.Lpad = (c->L + 7) / 8 * 8;
+  if (d.Lpad > edaa::kMaxLpad)
+    return set_err(c, EDAA_ERR_UNSUPPORTED, "band count above the compiled maximum (320)");
+  d.N = c->N;
+  d.Npad = c->Npad;
+  d.ntiles = d.Npad / edaa::kNP;
+  d.nslices = std::min(edaa::kMaxSlices, (d.ntiles + edaa::kTilesPerSlice - 1) / edaa::kTilesPerSlice);
+  d.M = static_cast<int>(prm->runs);
+  d.p = static_cast<int>(p);
+  d.RC = std::max(1, std::min(32 / d.p, d.M));
+  d.QCpad = (d.RC * d.p + 7) / 8 * 8;
+  d.NCH = (d.M + d.RC - 1) / d.RC;
+  d.Qs = d.NCH * d.QCpad;
+  d.Lrows = d.Lpad + d.QCpad;
+  d.K1 = static_cast<int>(prm->inner_iters_a);
+  *out = d;
+  return EDAA_OK;
+}
+
+int alloc_solve(edaa_ctx* c, const Dims& d, size_t T) {
+  const size_t mpn = static_cast<size_t>(d.M) * d.p * d.Npad * 8;
+  const size_t lq = static_cast<size_t>(d.Lpad) * d.Qs * 8;
+  const size_t qq = static_cast<size_t>(d.QCpad) * d.Qs * 8;
+  const size_t S = d.nslices;
+  c->fit_blocks = std::max(1, std::min(64, (d.N + 255) / 256));
+  EDAA_CUDA(c, ensure(c->A, mpn));
+  EDAA_CUDA(c, ensure(c->Lg, mpn));
+  EDAA_CUDA(c, ensure(c->Bv, mpn));
+  EDAA_CUDA(c, ensure(c->Y, lq));
+  EDAA_CUDA(c, ensure(c->Z, lq));
+  EDAA_CUDA(c, ensure(c->XAt, lq));
+  EDAA_CUDA(c, ensure(c->AAt, qq));
+  EDAA_CUDA(c, ensure(c->Gbuf, qq));
+  EDAA_CUDA(c, ensure(c->colm, d.Qs * 8));
+  EDAA_CUDA(c, ensure(c->colS, d.Qs * 8));
+  EDAA_CUDA(c, ensure(c->collogS, d.Qs * 8));
+  EDAA_CUDA(c, ensure(c->eta_a, d.M * 8));
+  EDAA_CUDA(c, ensure(c->eta_b, d.M * 8));
+  EDAA_CUDA(c, ensure(c->gamma, d.M * 8));
+  EDAA_CUDA(c, ensure(c->trace, static_cast<size_t>(d.M) * (T + 1) * 8));
+  EDAA_CUDA(c, ensure(c->part_C, S * d.Lrows * d.Qs * 8));
+  EDAA_CUDA(c, ensure(c->part_m, S * d.Qs * 8));
+  EDAA_CUDA(c, ensure(c->part_S, S * d.Qs * 8));
+  EDAA_CUDA(c, ensure(c->part_obj, S * d.M * 8));
+  EDAA_CUDA(c, ensure(c->E, static_cast<size_t>(d.M) * d.Lpad * d.p * 8));
+  EDAA_CUDA(c, ensure(c->fit, d.M * 8));
+  EDAA_CUDA(c, ensure(c->mu, d.M * 8));
+  EDAA_CUDA(c, ensure(c->part_fit, static_cast<size_t>(d.M) * c->fit_blocks * 8));
+  EDAA_CUDA(c, ensure(c->seeds, d.M * 8));
+  EDAA_CUDA(c, ensure(c->fail_key, d.M * 8));
+  EDAA_CUDA(c, ensure(c->fail_code, d.M * 4));
+  EDAA_CUDA(c, ensure(c->fail_value, d.M * 8));
+  EDAA_CUDA(c, ensure(c->cand, d.M));
+  EDAA_CUDA(c, ensure(c->selected, 8));
+  EDAA_CUDA(c, ensure(c->fit_min, 8));
+  return EDAA_OK;
+}
+
+edaa::PassArgs pass_args(edaa_ctx* c, int t, const double* W) {
+  edaa::PassArgs a{};
+  a.d = c->d;
+  a.t = t;
+  a.X = c->X;
+  a.xnorm = c->xnorm;
+  a.W = W;
+  a.A = P<double>(c->A);
+  a.Lg = P<double>(c->Lg);
+  a.colm = P<double>(c->colm);
+  a.collogS = P<double>(c->collogS);
+  a.Gbuf = P<double>(c->Gbuf);
+  a.eta_a = P<double>(c->eta_a);
+  a.eta_b = P<double>(c->eta_b);
+  a.seeds = P<uint64_t>(c->seeds);
+  a.part_C = P<double>(c->part_C);
+  a.part_m = P<double>(c->part_m);
+  a.part_S = P<double>(c->part_S);
+  a.part_obj = P<double>(c->part_obj);
+  a.fail_key = P<unsigned long long>(c->fail_key);
+  a.observe_A = nullptr;
+  return a;
+}
+
+edaa::CombineArgs combine_args(edaa_ctx* c, int t, int mode, int trace_index) {
+  edaa::CombineArgs a{};
+  a.d = c->d;
+  a.t = t;
+  a.mode = mode;
+  a.part_C = P<double>(c->part_C);
+  a.part_m = P<double>(c->part_m);
+  a.part_S = P<double>(c->part_S);
+  a.part_obj = P<double>(c->part_obj);
+  a.Y = P<double>(c->Y);
+  a.colm = P<double>(c->colm);
+  a.colS = P<double>(c->colS);
+  a.collogS = P<double>(c->collogS);
+  a.XAt = P<double>(c->XAt);
+  a.AAt = P<double>(c->AAt);
+  a.trace = P<double>(c->trace);
+  a.trace_stride = static_cast<int>(c->T + 1);
+  a.trace_index = trace_index;
+  a.fail_key = P<unsigned long long>(c->fail_key);
+  return a;
+}
+
+edaa::PostArgs post_args(edaa_ctx* c, int mode) {
+  edaa::PostArgs a{};
+  a.d = c->d;
+  a.mode = mode;
+  a.Y = P<double>(c->Y);
+  a.XAt = P<double>(c->XAt);
+  a.AAt = P<double>(c->AAt);
+  a.Z = P<double>(c->Z);
+  a.Gbuf = P<double>(c->Gbuf);
+  a.gamma = P<double>(c->gamma);
+  a.eta_a = P<double>(c->eta_a);
+  a.eta_b = P<double>(c->eta_b);
+  a.fail_code = P<int>(c->fail_code);
+  a.fail_value = P<double>(c->fail_value);
+  return a;
+}
+
+#define EDAA_LAUNCH(ctx, call)                                      \
+  do {                                                              \
+    cudaError_t e_ = (call);                                        \
+    if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #call);      \
+  } while (0)
+
+// Observer hooks used by edaa_solve_observed (null in the batched path).
+struct ObserveHook {
+  edaa_observer_fn fn = nullptr;
+  void* user = nullptr;
+  std::vector<double> a_host, b_host, obs;
+};
+
+int download_b(edaa_ctx* c, ObserveHook* h) {
+  const Dims& d = c->d;
+  EDAA_LAUNCH(c, edaa::launch_materialize_b(P<double>(c->Lg), P<double>(c->colm), P<double>(c->colS),
+                                            P<double>(c->Bv), d, c->stream));
+  std::vector<double> bv(static_cast<size_t>(d.p) * d.Npad);
+  EDAA_CUDA(c, cudaMemcpyAsync(bv.data(), c->Bv.p, bv.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  h->b_host.resize(static_cast<size_t>(d.N) * d.p);
+  for (int j = 0; j < d.N; ++j)
+    for (int i = 0; i < d.p; ++i) h->b_host[static_cast<size_t>(j) * d.p + i] = bv[static_cast<size_t>(i) * d.Npad + j];
+  return EDAA_OK;
+}
+
+bool all_finite(const double* v, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
+  Dims d{};
+  int rc = make_dims(c, prm, &d);
+  if (rc) return rc;
+  c->d = d;
+  c->T = prm->outer_iters;
+  c->solved = false;
+  rc = alloc_solve(c, d, c->T);
+  if (rc) return rc;
+  cudaStream_t st = c->stream;
+  EDAA_CUDA(c, cudaMemcpyAsync(c->seeds.p, prm->seeds, d.M * 8, cudaMemcpyHostToDevice, st));
+  EDAA_CUDA(c, cudaMemcpyAsync(c->gamma.p, prm->gammas, d.M * 8, cudaMemcpyHostToDevice, st));
+  EDAA_CUDA(c, cudaMemsetAsync(c->fail_key.p, 0xFF, d.M * 8, st));
+  EDAA_CUDA(c, cudaMemsetAsync(c->fail_code.p, 0, d.M * 4, st));
+  EDAA_CUDA(c, cudaMemsetAsync(c->fail_value.p, 0, d.M * 8, st));
+  // Zero the band-padding rows of Y/Z (and everything else) once.
+  EDAA_CUDA(c, cudaMemsetAsync(c->Y.p, 0, static_cast<size_t>(d.Lpad) * d.Qs * 8, st));
+  EDAA_CUDA(c, cudaMemsetAsync(c->Z.p, 0, static_cast<size_t>(d.Lpad) * d.Qs * 8, st));
+  EDAA_CUDA(c, cudaMemsetAsync(c->Gbuf.p, 0, static_cast<size_t>(d.QCpad) * d.Qs * 8, st));
+  EDAA_CUDA(c, cudaMemsetAsync(c->E.p, 0, static_cast<size_t>(d.M) * d.Lpad * d.p * 8, st));
+  EDAA_CUDA(c, cudaMemsetAsync(c->Lg.p, 0, static_cast<size_t>(d.M) * d.p * d.Npad * 8, st));
+  k_fill_a<<<592, 256, 0, st>>>(P<double>(c->A), d.M, d.p, d.N, d.Npad);
+  EDAA_LAUNCH(c, cudaGetLastError());
+
+  if (hook) {
+    EDAA_CUDA(c, ensure(c->obsA, static_cast<size_t>(d.K1) * d.p * d.Npad * 8));
+    hook->obs.resize(static_cast<size_t>(d.K1) * d.p * d.Npad);
+    hook->a_host.resize(static_cast<size_t>(d.p) * d.N);
+  }
+
+  // ---- initialisation: B⁰, Y⁰ = X·B⁰, η, G ----
+  {
+    edaa::PassArgs pa = pass_args(c, 0, nullptr);
+    EDAA_LAUNCH(c, edaa::launch_pass(edaa::kModeInit, pa, st));
+    EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, 0, edaa::kModeInit, 0), st));
+    EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostInit), st));
+  }
+  for (size_t t = 1; t <= c->T; ++t) {
+    const int ti = static_cast<int>(t);
+    edaa::PassArgs pa = pass_args(c, ti, P<double>(c->Y));
+    if (hook) pa.observe_A = P<double>(c->obsA);
+    EDAA_LAUNCH(c, edaa::launch_pass(edaa::kModeA, pa, st));
+    EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeA, ti - 1), st));
+    EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostZ), st));
+    if (hook) {
+      // B is fixed through the A block; snapshot it once, then replay the K1 iterates.
+      rc = download_b(c, hook);
+      if (rc) return rc;
+      EDAA_CUDA(c, cudaMemcpyAsync(hook->obs.data(), c->obsA.p, hook->obs.size() * 8,
+                                   cudaMemcpyDeviceToHost, st));
+      EDAA_CUDA(c, cudaStreamSynchronize(st));
+      for (int k = 0; k < d.K1; ++k) {
+        for (int i = 0; i < d.p; ++i)
+          std::memcpy(hook->a_host.data() + static_cast<size_t>(i) * d.N,
+                      hook->obs.data() + (static_cast<size_t>(k) * d.p + i) * d.Npad, d.N * 8);
+        if (!all_finite(hook->a_host.data(), hook->a_host.size())) break;  // run failed here
+        hook->fn(t, 'A', static_cast<size_t>(k + 1), hook->a_host.data(), hook->b_host.data(),
+                 d.p, d.N, hook->user);
+      }
+    }
+    for (size_t k = 1; k <= prm->inner_iters_b; ++k) {
+      edaa::PassArgs pb = pass_args(c, ti, P<double>(c->Z));
+      EDAA_LAUNCH(c, edaa::launch_pass(edaa::kModeB, pb, st));
+      EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0), st));
+      const bool last = (k == prm->inner_iters_b);
+      EDAA_LAUNCH(c, edaa::launch_post(post_args(c, last ? edaa::kPostG : edaa::kPostZ), st));
+      if (hook) {
+        rc = download_b(c, hook);
+        if (rc) return rc;
+        if (!all_finite(hook->b_host.data(), hook->b_host.size())) break;
+        hook->fn(t, 'B', k, hook->a_host.data(), hook->b_host.data(), d.p, d.N, hook->user);
+      }
+    }
+    if (hook) {
+      unsigned long long key = 0;
+      int code = 0;
+      EDAA_CUDA(c, cudaMemcpyAsync(&key, c->fail_key.p, 8, cudaMemcpyDeviceToHost, st));
+      EDAA_CUDA(c, cudaMemcpyAsync(&code, c->fail_code.p, 4, cudaMemcpyDeviceToHost, st));
+      EDAA_CUDA(c, cudaStreamSynchronize(st));
+      if (key != ~0ull || code != 0) break;  // the reference stops at the first failure
+    }
+  }
+  // ---- finalisation: trace[T], B̂, Ê = X·B̂, fit, coherence ----
+  {
+    edaa::PassArgs po = pass_args(c, static_cast<int>(c->T), P<double>(c->Y));
+    EDAA_LAUNCH(c, edaa::launch_pass(edaa::kModeObj, po, st));
+    edaa::CombineArgs co = combine_args(c, static_cast<int>(c->T), edaa::kModeObj, static_cast<int>(c->T));
+    EDAA_LAUNCH(c, edaa::launch_combine(co, st));
+    EDAA_LAUNCH(c, edaa::launch_materialize_b(P<double>(c->Lg), P<double>(c->colm), P<double>(c->colS),
+                                              P<double>(c->Bv), d, st));
+    EDAA_LAUNCH(c, edaa::launch_strict_e(c->X, P<double>(c->Bv), P<double>(c->E), d, st));
+    EDAA_LAUNCH(c, edaa::launch_fit(c->X, P<double>(c->E), P<double>(c->A), P<double>(c->part_fit),
+                                    P<double>(c->fit), c->fit_blocks, d, st));
+    EDAA_LAUNCH(c, edaa::launch_coherence(P<double>(c->E), P<double>(c->mu), d, st));
+  }
+  return EDAA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* edaa_version(void) { return "edaa-b200 0.1.0 (sm_100a, fp64 DMMA)"; }
+size_t edaa_max_endmembers(void) { return edaa::kMaxP; }
+size_t edaa_max_bands(void) { return edaa::kMaxLpad; }
+
+int edaa_create(int device, edaa_ctx** out) {
+  if (!out) return EDAA_ERR_INVALID;
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || device < 0 || device >= n) return EDAA_ERR_CUDA;
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return EDAA_ERR_CUDA;
+  edaa_ctx* c = new edaa_ctx();
+  c->device = device;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return EDAA_ERR_CUDA;
+  }
+  *out = c;
+  return EDAA_OK;
+}
+
+int edaa_destroy(edaa_ctx* c) {
+  if (!c) return EDAA_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  edaa_ctx::Buf* bufs[] = {&c->A, &c->Lg, &c->Bv, &c->Y, &c->Z, &c->XAt, &c->AAt, &c->Gbuf,
+                           &c->colm, &c->colS, &c->collogS, &c->eta_a, &c->eta_b, &c->gamma,
+                           &c->trace, &c->part_C, &c->part_m, &c->part_S, &c->part_obj, &c->E,
+                           &c->fit, &c->mu, &c->part_fit, &c->seeds, &c->fail_key, &c->fail_code,
+                           &c->fail_value, &c->cand, &c->selected, &c->fit_min, &c->obsA};
+  for (auto* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (c->X) cudaFree(c->X);
+  if (c->xnorm) cudaFree(c->xnorm);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return EDAA_OK;
+}
+
+const char* edaa_last_error(const edaa_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void* edaa_stream(edaa_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels) {
+  if (bands < 1 || pixels < 1)
+    return set_err(c, EDAA_ERR_INVALID, "image: needs at least one band and one pixel");
+  if (pixels > (1u << 30) || bands > (1u << 20)) return set_err(c, EDAA_ERR_UNSUPPORTED, "image too large");
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  c->L = static_cast<int>(bands);
+  c->N = static_cast<int>(pixels);
+  c->Npad = (c->N + edaa::kNP - 1) / edaa::kNP * edaa::kNP;
+  const size_t xb = static_cast<size_t>(c->L) * c->Npad * 4;
+  if (c->x_cap < xb) {
+    if (c->X) cudaFree(c->X);
+    c->X = nullptr;
+    c->x_cap = 0;
+    EDAA_CUDA(c, cudaMalloc(&c->X, xb));
+    c->x_cap = xb;
+  }
+  const size_t nb = static_cast<size_t>(c->Npad) * 8;
+  if (c->xn_cap < nb) {
+    if (c->xnorm) cudaFree(c->xnorm);
+    c->xnorm = nullptr;
+    c->xn_cap = 0;
+    EDAA_CUDA(c, cudaMalloc(&c->xnorm, nb));
+    c->xn_cap = nb;
+  }
+  c->solved = false;
+  return EDAA_OK;
+}
+
+int edaa_set_image_host(edaa_ctx* c, const float* x, size_t bands, size_t pixels) {
+  if (!c || !x) return set_err(c, EDAA_ERR_INVALID, "null argument");
+  int rc = prepare_image(c, bands, pixels);
+  if (rc) return rc;
+  EDAA_CUDA(c, cudaMemcpy2DAsync(c->X, static_cast<size_t>(c->Npad) * 4, x, pixels * 4, pixels * 4,
+                                 bands, cudaMemcpyHostToDevice, c->stream));
+  if (c->Npad > c->N)
+    EDAA_CUDA(c, cudaMemset2DAsync(c->X + c->N, static_cast<size_t>(c->Npad) * 4, 0,
+                                   static_cast<size_t>(c->Npad - c->N) * 4, bands, c->stream));
+  Dims d{};
+  d.L = c->L;
+  d.N = c->N;
+  d.Npad = c->Npad;
+  EDAA_LAUNCH(c, edaa::launch_xnorm(c->X, c->xnorm, d, c->stream));
+  return EDAA_OK;
+}
+
+int edaa_set_image_device(edaa_ctx* c, const float* x, size_t bands, size_t pixels, size_t ld) {
+  if (!c || !x) return set_err(c, EDAA_ERR_INVALID, "null argument");
+  if (ld < pixels) return set_err(c, EDAA_ERR_INVALID, "row pitch smaller than the pixel count");
+  int rc = prepare_image(c, bands, pixels);
+  if (rc) return rc;
+  k_pad_copy<<<592, 256, 0, c->stream>>>(x, ld, c->X, c->L, c->N, c->Npad);
+  EDAA_LAUNCH(c, cudaGetLastError());
+  Dims d{};
+  d.L = c->L;
+  d.N = c->N;
+  d.Npad = c->Npad;
+  EDAA_LAUNCH(c, edaa::launch_xnorm(c->X, c->xnorm, d, c->stream));
+  return EDAA_OK;
+}
+
+int edaa_solve_async(edaa_ctx* c, const edaa_solve_params* prm) {
+  if (!c) return EDAA_ERR_INVALID;
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  return solve_impl(c, prm, nullptr);
+}
+
+int edaa_finish(edaa_ctx* c) {
+  if (!c) return EDAA_ERR_INVALID;
+  const Dims& d = c->d;
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->h_fit.resize(d.M);
+  c->h_mu.resize(d.M);
+  c->h_eta_a.resize(d.M);
+  c->h_eta_b.resize(d.M);
+  c->h_fail_value.resize(d.M);
+  c->h_fail_code.resize(d.M);
+  c->h_fail_key.resize(d.M);
+  c->h_trace.resize(static_cast<size_t>(d.M) * (c->T + 1));
+  EDAA_CUDA(c, cudaMemcpy(c->h_fit.data(), c->fit.p, d.M * 8, cudaMemcpyDeviceToHost));
+  EDAA_CUDA(c, cudaMemcpy(c->h_mu.data(), c->mu.p, d.M * 8, cudaMemcpyDeviceToHost));
+  EDAA_CUDA(c, cudaMemcpy(c->h_eta_a.data(), c->eta_a.p, d.M * 8, cudaMemcpyDeviceToHost));
+  EDAA_CUDA(c, cudaMemcpy(c->h_eta_b.data(), c->eta_b.p, d.M * 8, cudaMemcpyDeviceToHost));
+  EDAA_CUDA(c, cudaMemcpy(c->h_fail_value.data(), c->fail_value.p, d.M * 8, cudaMemcpyDeviceToHost));
+  EDAA_CUDA(c, cudaMemcpy(c->h_fail_code.data(), c->fail_code.p, d.M * 4, cudaMemcpyDeviceToHost));
+  EDAA_CUDA(c, cudaMemcpy(c->h_fail_key.data(), c->fail_key.p, d.M * 8, cudaMemcpyDeviceToHost));
+  EDAA_CUDA(c, cudaMemcpy(c->h_trace.data(), c->trace.p, c->h_trace.size() * 8, cudaMemcpyDeviceToHost));
+  c->solved = true;
+  return EDAA_OK;
+}
+
+int edaa_solve(edaa_ctx* c, const edaa_solve_params* prm) {
+  int rc = edaa_solve_async(c, prm);
+  if (rc) return rc;
+  return edaa_finish(c);
+}
+
+int edaa_run_record_get(edaa_ctx* c, size_t run, edaa_run_record* out) {
+  if (!c || !out) return EDAA_ERR_INVALID;
+  if (!c->solved) return set_err(c, EDAA_ERR_STATE, "no finished solve");
+  if (run >= static_cast<size_t>(c->d.M)) return set_err(c, EDAA_ERR_INVALID, "run index out of range");
+  std::memset(out, 0, sizeof *out);
+  out->fit_l1 = c->h_fit[run];
+  out->coherence = c->h_mu[run];
+  out->eta_a = c->h_eta_a[run];
+  out->eta_b = c->h_eta_b[run];
+  int code = c->h_fail_code[run];
+  size_t outer = 0;
+  if (code == EDAA_RUN_OK && c->h_fail_key[run] != ~0ull) {
+    outer = static_cast<size_t>(c->h_fail_key[run] >> 1);
+    code = (c->h_fail_key[run] & 1ull) ? EDAA_RUN_NONFINITE_B : EDAA_RUN_NONFINITE_A;
+  }
+  out->fail_code = code;
+  out->fail_outer = outer;
+  out->ok = code == EDAA_RUN_OK;
+  const std::string msg = run_message(code, outer, c->h_fail_value[run]);
+  std::snprintf(out->message, sizeof out->message, "%s", msg.c_str());
+  return EDAA_OK;
+}
+
+int edaa_traces(edaa_ctx* c, double* out) {
+  if (!c || !out) return EDAA_ERR_INVALID;
+  if (!c->solved) return set_err(c, EDAA_ERR_STATE, "no finished solve");
+  std::memcpy(out, c->h_trace.data(), c->h_trace.size() * 8);
+  return EDAA_OK;
+}
+
+int edaa_factors(edaa_ctx* c, size_t run, double* a, double* b, double* e) {
+  if (!c) return EDAA_ERR_INVALID;
+  if (!c->solved) return set_err(c, EDAA_ERR_STATE, "no finished solve");
+  const Dims& d = c->d;
+  if (run >= static_cast<size_t>(d.M)) return set_err(c, EDAA_ERR_INVALID, "run index out of range");
+  const size_t pN = static_cast<size_t>(d.p) * d.Npad;
+  if (a) {
+    EDAA_CUDA(c, cudaMemcpy2D(a, d.N * 8, P<double>(c->A) + run * pN, d.Npad * 8, d.N * 8, d.p,
+                              cudaMemcpyDeviceToHost));
+  }
+  if (b) {  // device keeps B column-major per run; the reference layout is N×p
+    std::vector<double> tmp(pN);
+    EDAA_CUDA(c, cudaMemcpy(tmp.data(), P<double>(c->Bv) + run * pN, pN * 8, cudaMemcpyDeviceToHost));
+    for (int j = 0; j < d.N; ++j)
+      for (int i = 0; i < d.p; ++i) b[static_cast<size_t>(j) * d.p + i] = tmp[static_cast<size_t>(i) * d.Npad + j];
+  }
+  if (e) {
+    EDAA_CUDA(c, cudaMemcpy(e, P<double>(c->E) + run * d.Lpad * d.p, static_cast<size_t>(d.L) * d.p * 8,
+                            cudaMemcpyDeviceToHost));
+  }
+  return EDAA_OK;
+}
+
+int edaa_select(edaa_ctx* c, double fit_slack, uint8_t* cand, size_t* selected, double* fit_min) {
+  if (!c || !cand || !selected || !fit_min) return EDAA_ERR_INVALID;
+  if (!c->solved) return set_err(c, EDAA_ERR_STATE, "no finished solve");
+  if (!std::isfinite(fit_slack) || fit_slack < 1.0)
+    return set_err(c, EDAA_ERR_INVALID, "fit slack must be at least 1");
+  const Dims& d = c->d;
+  EDAA_LAUNCH(c, edaa::launch_select(P<double>(c->fit), P<double>(c->mu), P<int>(c->fail_code),
+                                     P<unsigned long long>(c->fail_key), d.M, fit_slack,
+                                     P<unsigned char>(c->cand), P<long long>(c->selected),
+                                     P<double>(c->fit_min), c->stream));
+  long long sel = -1;
+  EDAA_CUDA(c, cudaMemcpyAsync(cand, c->cand.p, d.M, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaMemcpyAsync(&sel, c->selected.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaMemcpyAsync(fit_min, c->fit_min.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (sel < 0) return set_err(c, EDAA_ERR_ALL_FAILED, "every run failed");
+  *selected = static_cast<size_t>(sel);
+  return EDAA_OK;
+}
+
+int edaa_solve_observed(edaa_ctx* c, const edaa_solve_params* prm, edaa_observer_fn fn, void* user) {
+  if (!c || !fn) return set_err(c, EDAA_ERR_INVALID, "null argument");
+  if (!prm || prm->runs != 1) return set_err(c, EDAA_ERR_INVALID, "observed mode takes exactly one run");
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  ObserveHook hook;
+  hook.fn = fn;
+  hook.user = user;
+  int rc = solve_impl(c, prm, &hook);
+  if (rc) return rc;
+  return edaa_finish(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// Internal declarations shared by the EDAA sm_100a kernels and the C-ABI.
+//
+// Data layout in HBM (one device, a batch of M runs, p endmembers each):
+//   X       fp32 [L][Npad]       band-major, pixels contiguous (BSQ plane order,
+//                                reference layout L×N, envi.cpp:160-174); zero
+//                                padded to Npad = ceil(N/64)·64.
+//   xnorm   fp64 [Npad]          ‖x_j‖² (fp64 sum of the fp32 values).
+//   A       fp64 [M][p][Npad]    abundances, run-major then endmember (rows of
+//                                the reference p×N matrix, solver.hpp:29-38).
+//   Lg      fp64 [M][p][Npad]    contribution LOGITS ℓ; B = softmax over
+//                                pixels: b_j = exp(ℓ_j − m)/S with the column
+//                                normaliser (m, S) kept in colm/colS.
+//   Columns of the batch live in a chunk-padded space of Qs = NCH·QCpad slots:
+//   chunk k holds runs [k·RC, k·RC+RC), run-local column i at k·QCpad+rl·p+i.
+//   Y, Z, XAt  fp64 [Lpad][Qs]   Y = X·B, Z = XAᵀ − Y·AAᵀ, XAt = X·Aᵀ.
+//   AAt, G     fp64 [QCpad][Qs]  per-run p×p blocks on the chunk diagonal.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace edaa {
+
+constexpr int kThreads = 256;   // 8 warps per CTA
+constexpr int kNP = 64;         // pixels per tile
+constexpr int kXST = kNP + 8;   // fp32 X tile row stride (bank-conflict free DMMA B-frags)
+constexpr int kSST = kNP + 4;   // fp64 weight tile row stride
+constexpr int kMaxSlices = 296; // 2 × 148 SMs
+constexpr int kTilesPerSlice = 4;
+constexpr int kMaxP = 16;
+constexpr int kMaxLpad = 320;
+constexpr double kLogFloorValue = 1e-30;  // solver.cpp:15
+
+enum PassMode : int { kModeInit = 0, kModeA = 1, kModeB = 2, kModeObj = 3 };
+
+// Failure codes per run (map to the reference's archetype::Error messages).
+enum FailCode : int {
+  kOk = 0,
+  kNonFiniteA = 1,       // "non-finite abundance iterate at outer iteration t"  solver.cpp:74
+  kNonFiniteB = 2,       // "non-finite contribution iterate at outer iteration t"
+  kDegenerateInit = 3,   // "degenerate initialization: X·B0 is zero"  solver.cpp:141
+  kSpectralBad = 4,      // "spectral_norm: matrix must be finite and nonzero"  matrix.cpp:151
+  kSpectralNoConv = 5,   // "spectral_norm: no convergence after ..."  matrix.cpp:186-189
+};
+
+struct Dims {
+  int L, Lpad, N, Npad;
+  int ntiles, nslices;
+  int M, p, RC, QCpad, NCH, Qs;
+  int Lrows;  // Lpad + QCpad (A-pass pseudo rows carry AAᵀ)
+  int K1;
+};
+
+struct PassArgs {
+  Dims d;
+  int t;  // outer iteration (1-based); 0 for init
+  const float* X;
+  const double* xnorm;
+  const double* W;        // Y (A/OBJ pass) or Z (B pass), [Lpad][Qs]
+  double* A;              // [M][p][Npad]
+  double* Lg;             // [M][p][Npad]
+  const double* colm;     // [Qs] normaliser max of the current logits
+  const double* collogS;  // [Qs] log of the normaliser sum
+  const double* Gbuf;     // [QCpad][Qs]
+  const double* eta_a;    // [M]
+  const double* eta_b;    // [M]
+  const uint64_t* seeds;  // [M]
+  double* part_C;         // [nslices][Lrows][Qs]
+  double* part_m;         // [nslices][Qs]
+  double* part_S;         // [nslices][Qs]
+  double* part_obj;       // [nslices][M]
+  unsigned long long* fail_key;  // [M]  min over (t<<1 | block)
+  double* observe_A;      // optional [K1][p][Npad] inner iterates (M == 1 observed mode)
+};
+
+struct CombineArgs {
+  Dims d;
+  int t;
+  int mode;  // kModeA: plain sums (XAt, AAt, objective); kModeB/kModeInit: LSE combine into Y
+  const double* part_C;
+  const double* part_m;
+  const double* part_S;
+  const double* part_obj;
+  double* Y;        // B/init output
+  double* colm;
+  double* colS;
+  double* collogS;
+  double* XAt;      // A output
+  double* AAt;      // A output [QCpad][Qs]
+  double* trace;    // [M][T+1]
+  int trace_stride;
+  int trace_index;
+  unsigned long long* fail_key;
+};
+
+enum PostMode : int { kPostZ = 0, kPostG = 1, kPostInit = 2 };
+
+struct PostArgs {
+  Dims d;
+  int mode;
+  const double* Y;
+  const double* XAt;
+  const double* AAt;
+  double* Z;
+  double* Gbuf;
+  const double* gamma;  // [M]
+  double* eta_a;
+  double* eta_b;
+  int* fail_code;       // [M]
+  double* fail_value;   // [M]
+};
+
+// Kernel launchers (edaa_kernels.cu). All enqueue on `st`; none synchronise.
+cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st);
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
+cudaError_t launch_post(const PostArgs& a, cudaStream_t st);
+cudaError_t launch_xnorm(const float* X, double* xnorm, const Dims& d, cudaStream_t st);
+cudaError_t launch_materialize_b(const double* Lg, const double* colm, const double* colS,
+                                 double* Bv, const Dims& d, cudaStream_t st);
+cudaError_t launch_strict_e(const float* X, const double* Bv, double* E, const Dims& d,
+                            cudaStream_t st);
+cudaError_t launch_fit(const float* X, const double* E, const double* A, double* part_fit,
+                       double* fit, int fit_blocks, const Dims& d, cudaStream_t st);
+cudaError_t launch_coherence(const double* E, double* mu, const Dims& d, cudaStream_t st);
+cudaError_t launch_select(const double* fit, const double* mu, const int* fail_code,
+                          const unsigned long long* fail_key, int M, double slack,
+                          unsigned char* cand, long long* selected, double* fit_min,
+                          cudaStream_t st);
+size_t pass_smem_bytes(int mode, const Dims& d);
+
+}  // namespace edaa

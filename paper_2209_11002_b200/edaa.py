@@ -1,0 +1,350 @@
+"""Python surface of the B200 EDAA path, mirroring the reference C++ API.
+
+Names, argument meaning and error behaviour follow
+``/root/reference/proj/include/archetype/{solver,ensemble,prng}.hpp``:
+
+=====================  ==========================================================
+``SolverConfig``       solver.hpp:15-24 (validate: solver.cpp:103-111)
+``RunResult``          solver.hpp:29-38
+``run``                solver.hpp:81 / solver.cpp:190-238  → one-run batch on the GPU
+``EnsembleConfig``     ensemble.hpp:15-29 (validate: ensemble.cpp:17-27)
+``RunRecord``          ensemble.hpp:31-40
+``SelectionReport``    ensemble.hpp:42-47
+``run_ensemble``       ensemble.hpp:68-69 / ensemble.cpp:108-167 → ONE batched solve
+``select_runs``        ensemble.hpp:63 / ensemble.cpp:71-94
+``sample_gamma``       ensemble.hpp:58 / ensemble.cpp:62-69
+``Prng``               prng.hpp:11-30 (SplitMix64, bit-exact)
+=====================  ==========================================================
+
+Every solve runs in the sm_100a kernels behind ``include/edaa_b200.h``; there
+is no CPU fallback (a missing library or GPU raises :class:`EdaaError`).
+Errors carry the reference's ``archetype::Error`` messages.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import EdaaError, RunRecordC, SolveParams
+
+DEFAULT_GAMMAS = (0.125, 0.25, 0.5, 1.0, 2.0, 4.0, 8.0)  # ensemble.hpp:18
+_MASK = (1 << 64) - 1
+
+
+class Prng:
+    """SplitMix64 with the reference's unit mapping (prng.hpp:15-26)."""
+
+    def __init__(self, seed: int):
+        self.state = int(seed) & _MASK
+
+    def next_u64(self) -> int:
+        self.state = (self.state + 0x9E3779B97F4A7C15) & _MASK
+        z = self.state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK
+        return z ^ (z >> 31)
+
+    def next_unit(self) -> float:
+        return float(self.next_u64() >> 11) * 2.0 ** -53
+
+
+def sample_gamma(rng: Prng, gamma_set: Sequence[float]) -> float:
+    """index = floor(u·|S|), clamped (ensemble.cpp:62-69)."""
+    if len(gamma_set) == 0:
+        raise EdaaError("step factor set is empty")
+    idx = int(rng.next_unit() * float(len(gamma_set)))
+    return gamma_set[min(idx, len(gamma_set) - 1)]
+
+
+@dataclass
+class SolverConfig:
+    endmembers: int = 0
+    outer_iters: int = 100
+    inner_iters_a: int = 5
+    inner_iters_b: int = 5
+    gamma: float = 1.0
+    seed: int = 0
+
+    def validate(self):
+        if self.endmembers < 2:
+            raise EdaaError("solver config: endmember count must be at least 2")
+        if self.outer_iters < 1 or self.inner_iters_a < 1 or self.inner_iters_b < 1:
+            raise EdaaError("solver config: iteration counts must be at least 1")
+        if not (self.gamma > 0.0) or not math.isfinite(self.gamma):
+            raise EdaaError("solver config: step factor gamma must be positive")
+
+
+@dataclass
+class EnsembleConfig:
+    runs: int = 50
+    base_seed: int = 0
+    gamma_set: Sequence[float] = DEFAULT_GAMMAS
+    fit_slack: float = 1.05
+    solver: SolverConfig = field(default_factory=SolverConfig)
+    workers: int = 0  # accepted for API parity; the batch runs as one device launch
+
+    def validate(self):
+        if self.runs == 0:
+            raise EdaaError("ensemble needs at least one run")
+        if len(self.gamma_set) == 0:
+            raise EdaaError("step factor set is empty")
+        for g in self.gamma_set:
+            if not math.isfinite(g) or g <= 0.0:
+                raise EdaaError("step factors must be finite and positive")
+        if not math.isfinite(self.fit_slack) or self.fit_slack < 1.0:
+            raise EdaaError("fit slack must be at least 1")
+        self.solver.validate()
+
+
+@dataclass
+class RunResult:
+    endmembers: np.ndarray      # L×p
+    abundances: np.ndarray      # p×N
+    contributions: np.ndarray   # N×p
+    fit_l1: float
+    coherence: float
+    seed: int
+    gamma: float
+    objective_trace: np.ndarray  # T+1
+
+
+@dataclass
+class RunRecord:
+    index: int = 0
+    seed: int = 0
+    gamma: float = 0.0
+    fit_l1: float = 0.0
+    coherence: float = 0.0
+    wall_ms: float = 0.0
+    ok: bool = False
+    error: str = ""
+
+
+@dataclass
+class SelectionReport:
+    per_run: List[RunRecord]
+    candidate_set: List[int]
+    selected: int
+    fit_min: float
+
+
+def select_runs(per_run: List[RunRecord], fit_slack: float) -> SelectionReport:
+    """Algorithm 2's rule on given records (ensemble.cpp:71-94); bookkeeping over
+    M scalars.  The device path (run_ensemble) applies the same rule on the GPU."""
+    fit_min = math.inf
+    for rec in per_run:
+        if rec.ok:
+            fit_min = min(fit_min, rec.fit_l1)
+    if fit_min == math.inf:
+        raise EdaaError("every run failed")
+    cutoff = fit_slack * fit_min
+    cand = [rec.index for rec in per_run if rec.ok and rec.fit_l1 <= cutoff]
+    best = cand[0]
+    for idx in cand:
+        if per_run[idx].coherence < per_run[best].coherence:
+            best = idx
+    return SelectionReport(per_run, cand, best, fit_min)
+
+
+def validate_image(x) -> np.ndarray:
+    """HsiImage::validate (image.cpp:10-27) on the L×N data; returns fp32 X."""
+    arr = np.asarray(x)
+    if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
+        raise EdaaError("image: needs at least one band and one pixel")
+    if not np.all(np.isfinite(arr)):
+        raise EdaaError("image: non-finite reflectance")
+    if np.any(arr < 0):
+        raise EdaaError("image: negative reflectance")
+    return np.ascontiguousarray(arr, dtype=np.float32)
+
+
+class Device:
+    """One edaa_ctx (one CUDA device).  Not thread-safe."""
+
+    _cache = {}
+
+    @classmethod
+    def get(cls, device: int = 0) -> "Device":
+        if device not in cls._cache:
+            cls._cache[device] = Device(device)
+        return cls._cache[device]
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        rc = self.lib.edaa_create(int(device), C.byref(h))
+        if rc != 0:
+            raise EdaaError("edaa_create failed on device %d (rc=%d): no usable CUDA device; "
+                            "there is no CPU fallback" % (device, rc), rc)
+        self.h = h
+        self.device = device
+        self.L = self.N = 0
+        self.M = 0
+        self.T = 0
+        self.p = 0
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.edaa_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            raise EdaaError(self.lib.edaa_last_error(self.h).decode("utf-8", "replace"), rc)
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.edaa_stream(self.h) or 0)
+
+    # -- image ------------------------------------------------------------------
+    def set_image(self, x):
+        """x: host L×N array (copied H2D) or a CUDA tensor (copied D2D)."""
+        if hasattr(x, "is_cuda") and x.is_cuda:
+            import torch
+            if x.dtype != torch.float32 or x.dim() != 2 or x.stride(1) != 1:
+                raise EdaaError("device image must be a row-contiguous 2-D float32 tensor")
+            self._check(self.lib.edaa_set_image_device(self.h, C.c_void_p(x.data_ptr()),
+                                                       x.shape[0], x.shape[1], x.stride(0)))
+            self.L, self.N = int(x.shape[0]), int(x.shape[1])
+            return
+        xf = np.ascontiguousarray(x, dtype=np.float32)
+        self._x_keep = xf
+        self._check(self.lib.edaa_set_image_host(self.h, xf.ctypes.data_as(C.c_void_p),
+                                                 xf.shape[0], xf.shape[1]))
+        self.L, self.N = xf.shape
+
+    # -- solve ------------------------------------------------------------------
+    def _params(self, p, T, K1, K2, seeds, gammas):
+        self._seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        self._gammas = np.ascontiguousarray(gammas, dtype=np.float64)
+        prm = SolveParams(p, T, K1, K2, len(self._seeds),
+                          self._seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
+                          self._gammas.ctypes.data_as(C.POINTER(C.c_double)))
+        self.M, self.T, self.p = len(self._seeds), T, p
+        return prm
+
+    def solve_async(self, p, T, K1, K2, seeds, gammas):
+        self._prm = self._params(p, T, K1, K2, seeds, gammas)
+        self._check(self.lib.edaa_solve_async(self.h, C.byref(self._prm)))
+
+    def finish(self):
+        self._check(self.lib.edaa_finish(self.h))
+
+    def solve(self, p, T, K1, K2, seeds, gammas):
+        self.solve_async(p, T, K1, K2, seeds, gammas)
+        self.finish()
+
+    def solve_observed(self, p, T, K1, K2, seed, gamma, observer: Callable):
+        prm = self._params(p, T, K1, K2, [seed], [gamma])
+        N = self.N
+
+        def cb(outer, block, inner, a_ptr, b_ptr, pp, n, user):
+            a = np.ctypeslib.as_array(a_ptr, shape=(pp * n,)).reshape(pp, n).copy()
+            b = np.ctypeslib.as_array(b_ptr, shape=(n * pp,)).reshape(n, pp).copy()
+            observer(int(outer), block.decode() if isinstance(block, bytes) else block,
+                     int(inner), a, b)
+
+        fn = _lib.OBSERVER_FN(cb)
+        self._check(self.lib.edaa_solve_observed(self.h, C.byref(prm), fn, None))
+        del N
+
+    # -- results ----------------------------------------------------------------
+    def record(self, run: int) -> RunRecordC:
+        out = RunRecordC()
+        self._check(self.lib.edaa_run_record_get(self.h, run, C.byref(out)))
+        return out
+
+    def traces(self) -> np.ndarray:
+        out = np.zeros((self.M, self.T + 1))
+        self._check(self.lib.edaa_traces(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def factors(self, run: int):
+        A = np.zeros((self.p, self.N))
+        B = np.zeros((self.N, self.p))
+        E = np.zeros((self.L, self.p))
+        self._check(self.lib.edaa_factors(self.h, run, A.ctypes.data_as(C.c_void_p),
+                                          B.ctypes.data_as(C.c_void_p),
+                                          E.ctypes.data_as(C.c_void_p)))
+        return A, B, E
+
+    def select(self, fit_slack: float):
+        cand = np.zeros(self.M, dtype=np.uint8)
+        sel = C.c_size_t()
+        fmin = C.c_double()
+        rc = self.lib.edaa_select(self.h, fit_slack, cand.ctypes.data_as(C.c_void_p),
+                                  C.byref(sel), C.byref(fmin))
+        if rc == _lib.EDAA_ERR_ALL_FAILED:
+            raise EdaaError("every run failed", rc)
+        self._check(rc)
+        return [int(i) for i in np.flatnonzero(cand)], int(sel.value), fmin.value
+
+
+def _result(dev: Device, run_idx: int, seed: int, gamma: float, traces) -> RunResult:
+    A, B, E = dev.factors(run_idx)
+    rec = dev.record(run_idx)
+    return RunResult(E, A, B, rec.fit_l1, rec.coherence, seed, gamma, traces[run_idx].copy())
+
+
+def run(x, config: SolverConfig, observer: Optional[Callable] = None, device: int = 0) -> RunResult:
+    """Algorithm 1 for one run (solver.cpp:190-238) on the GPU.
+
+    observer(outer, block, inner, A, B) is called after every inner step, as the
+    reference's StepObserver (solver.hpp:69-77)."""
+    config.validate()
+    xf = validate_image(x)
+    dev = Device.get(device)
+    dev.set_image(xf)
+    args = (config.endmembers, config.outer_iters, config.inner_iters_a, config.inner_iters_b)
+    if observer is not None:
+        dev.solve_observed(*args, config.seed, config.gamma, observer)
+    else:
+        dev.solve(*args, [config.seed], [config.gamma])
+    rec = dev.record(0)
+    if not rec.ok:
+        raise EdaaError(rec.message.decode("utf-8"))
+    return _result(dev, 0, config.seed, config.gamma, dev.traces())
+
+
+def ensemble_plan(config: EnsembleConfig, first: int = 0, count: Optional[int] = None):
+    """Seeds and step factors of runs [first, first+count): seed = base + m, γ from
+    that seed's first draw (ensemble.cpp:123-127)."""
+    count = config.runs - first if count is None else count
+    seeds, gammas = [], []
+    for m in range(first, first + count):
+        s = (config.base_seed + m) & _MASK
+        seeds.append(s)
+        gammas.append(sample_gamma(Prng(s), config.gamma_set))
+    return seeds, gammas
+
+
+def run_ensemble(x, config: EnsembleConfig, device: int = 0):
+    """Algorithm 2 (ensemble.cpp:108-167): all M runs in ONE batched device solve,
+    then selection on the device.  Returns (selected RunResult, SelectionReport)."""
+    config.validate()
+    xf = validate_image(x)
+    dev = Device.get(device)
+    dev.set_image(xf)
+    seeds, gammas = ensemble_plan(config)
+    s = config.solver
+    t0 = time.perf_counter()
+    dev.solve(s.endmembers, s.outer_iters, s.inner_iters_a, s.inner_iters_b, seeds, gammas)
+    wall = (time.perf_counter() - t0) * 1e3
+    recs = []
+    for m in range(config.runs):
+        rc = dev.record(m)
+        recs.append(RunRecord(m, seeds[m], gammas[m], rc.fit_l1 if rc.ok else 0.0,
+                              rc.coherence if rc.ok else 0.0, wall, bool(rc.ok),
+                              rc.message.decode("utf-8")))
+    cand, sel, fmin = dev.select(config.fit_slack)
+    report = SelectionReport(recs, cand, sel, fmin)
+    return _result(dev, sel, seeds[sel], gammas[sel], dev.traces()), report
