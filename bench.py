@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: EDAA run-iterations/s (BASELINE.json "metric") on B200.
+
+A step is ONE full EDAA ensemble of the chosen BASELINE config — M runs × T=100
+outer iterations (K1 = K2 = 5) with model selection — batched in one device
+solve.  The default workload is cfg1 (Jasper-Ridge shape: L=198, N=100×100,
+p=4, M=50), the config the metric is quoted on; synthetic seeded data of that
+shape (paper_2209_11002_b200/synth.py).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config cfg1] [--impl ours|reference]
+
+* ``value``: run-iterations/s with X resident in HBM, device time (CUDA events
+  on the solver stream, L2 flushed with a 256 MB write before every timed
+  step), max over ranks; N>1 = weak scaling (each rank its own M runs, the
+  records gathered for one selection over all M·N runs).
+* ``e2e``: the same metric through the public API ``run_ensemble`` with the
+  image in pinned host memory: H2D of X, solve, selection and D2H of the
+  selected run's A/B/E inside the timed region.
+* ``roofline``: the dominant kernel (the B-step pass) against the fp64
+  tensor-pipe (DMMA) peak measured live on this GPU; its HBM side vs
+  MEASURED_PEAKS.json is reported alongside.
+* ``cpu_baseline``: the reference CPU solver (oracle/_ref, built from
+  /root/reference) on this host's cores, bounded sample (rank 0, N=1).
+* ``--impl reference``: the reference CPU implementation alone, timed per step
+  on a bounded sample of the same workload (all host threads).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EDAA run-iterations/sec (M runs x T outer iterations) at N,L,p"
+UNIT = "run-iterations/s"
+# Paper (PyTorch, RTX 2080 Ti) end-to-end ensemble times, BASELINE.md §1.
+PUBLISHED = {"cfg1": 50 * 100 / 9.6, "cfg2": 50 * 100 / 75.2}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--outer", type=int, default=100, help="T (default: the reference's 100)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def scene(cfg_name):
+    from paper_2209_11002_b200 import synth
+    spec = synth.CONFIGS[cfg_name]
+    x, _, _ = synth.generate(spec)
+    return spec, x
+
+
+# ----------------------------------------------------------------------------- reference arm
+def cpu_reference_sample(x, spec, T, runs=None, workers=None):
+    """Reference run_ensemble on the host cores: returns (seconds, run-iters done, kind, cores)."""
+    from oracle import Oracle, available_kinds
+    kind = "reference" if "reference" in available_kinds() else "port"
+    orc = Oracle(kind)
+    cores = workers or os.cpu_count() or 1
+    runs = runs or cores
+    xd = x.astype(np.float64)
+    t0 = time.perf_counter()
+    orc.run_ensemble(xd, spec.endmembers, M=runs, T=T, workers=cores)
+    return time.perf_counter() - t0, runs * T, kind, cores
+
+
+def cpu_baseline(x, spec):
+    """Bounded sample: M = cores concurrent runs at T=1 and T=4; the difference
+    removes the per-run setup, giving steady-state run-iterations/s."""
+    t1, _, kind, cores = cpu_reference_sample(x, spec, 1)
+    t4, _, _, _ = cpu_reference_sample(x, spec, 4)
+    value = cores * 3 / max(t4 - t1, 1e-9)
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": "%s shape, M=%d concurrent runs (one per core), T=4 minus T=1 "
+                      "(%.1f s + %.1f s wall)" % (spec.name, cores, t4, t1)}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    spec, x = scene(args.config)
+    cores = os.cpu_count() or 1
+    T = 2  # bounded sample per step: M = cores runs × 2 outer iterations
+    for _ in range(args.warmup):
+        cpu_reference_sample(x, spec, T)
+    times = []
+    kind = None
+    for _ in range(args.steps):
+        dt, its, kind, cores = cpu_reference_sample(x, spec, T)
+        times.append(dt)
+    total = sum(times)
+    value = cores * T * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(spec, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": "%s shape, M=%d runs (one per core) x T=%d per step, "
+                                   "run_ensemble with %d workers" % (spec.name, cores, T, cores)},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(spec, args, runs=None, T=None):
+    return {"workload": "%s: EDAA ensemble L=%d N=%d p=%d M=%d T=%d K1=K2=5 + model selection"
+                        % (spec.name, spec.bands, spec.pixels, spec.endmembers,
+                           runs or spec.runs, T or args.outer),
+            "bands": spec.bands, "pixels": spec.pixels, "endmembers": spec.endmembers,
+            "runs_per_gpu": runs or spec.runs, "outer_iters": T or args.outer,
+            "inner_iters": [5, 5], "l2_flush": "256 MB write before every timed step",
+            "parallelism": "ensemble runs sharded over GPUs (weak scaling)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    import torch
+    from paper_2209_11002_b200 import edaa
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    spec, x = scene(args.config)
+    L, N, p, M, T = spec.bands, spec.pixels, spec.endmembers, spec.runs, args.outer
+    dev = edaa.Device.get(local)
+    stream = torch.cuda.ExternalStream(dev.stream, device=torch.device("cuda", local))
+    x_dev = torch.from_numpy(x).to(f"cuda:{local}")
+    torch.cuda.synchronize()
+    dev.set_image(x_dev)
+    cfg = edaa.EnsembleConfig(runs=M * world, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
+    seeds, gammas = edaa.ensemble_plan(cfg, first=rank * M, count=M)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def gather_select():
+        recs = [dev.record(m) for m in range(M)]
+        fits = torch.tensor([r.fit_l1 for r in recs], dtype=torch.float64, device=x_dev.device)
+        mus = torch.tensor([r.coherence for r in recs], dtype=torch.float64, device=x_dev.device)
+        oks = torch.tensor([float(r.ok) for r in recs], dtype=torch.float64, device=x_dev.device)
+        if world > 1:
+            import torch.distributed as dist
+            allv = [torch.empty(3, M, dtype=torch.float64, device=x_dev.device) for _ in range(world)]
+            dist.all_gather(allv, torch.stack([fits, mus, oks]))
+            cat = torch.cat(allv, dim=1).cpu().numpy()
+        else:
+            cat = torch.stack([fits, mus, oks]).cpu().numpy()
+        records = [edaa.RunRecord(i, 0, 0.0, cat[0, i], cat[1, i], 0.0, bool(cat[2, i]), "")
+                   for i in range(cat.shape[1])]
+        return edaa.select_runs(records, cfg.fit_slack).selected
+
+    def one_step(timed):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        dev.solve_async(p, T, 5, 5, seeds, gammas)
+        dev.finish()
+        if world == 1:
+            dev.select(cfg.fit_slack)
+        else:
+            gather_select()
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(max(args.warmup, 3)):
+        one_step(False)
+    dev.profile_enable(True)
+    one_step(False)
+    prof = dev.profile()
+    dev.profile_enable(False)
+    sampler = ClockSampler(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    n0 = dev.launch_count()
+    times = [one_step(True) for _ in range(args.steps)]
+    launches = dev.launch_count() - n0
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    t_dev = sum(times)  # ms on this rank
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_dev], dtype=torch.float64, device=x_dev.device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    run_iters = M * world * T * args.steps
+    value = run_iters / (t_dev * 1e-3)
+
+    # ---- e2e through the public API (pinned host X; H2D + solve + select + D2H) ----
+    e2e = None
+    if not args.no_e2e and world == 1:
+        x_pin = torch.from_numpy(x).pin_memory().numpy()
+        ecfg = edaa.EnsembleConfig(runs=M, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
+        edaa.run_ensemble(x_pin, ecfg, device=local)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            edaa.run_ensemble(x_pin, ecfg, device=local)
+        dt = time.perf_counter() - t0
+        e2e = {"value": M * T * args.steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(x.nbytes + 16 * M),
+               "d2h_bytes_per_step": int(8 * (2 * p * N + L * p + (T + 1) * M + 4 * M) + M)}
+        dev.set_image(x_dev)
+
+    # ---- roofline of the dominant kernel (B-step pass) ----
+    peak64 = dev.fp64_peak_tflops()
+    ms_b, n_b = prof["B"]
+    ms_a, n_a = prof["A"]
+    launch_ms = ms_b / max(n_b, 1)
+    flops_b = 4.0 * L * N * p * M  # g = XᵀZ and Y = X·B, M runs per launch
+    bytes_b = 4.0 * L * N + 16.0 * p * N * M  # X once + logits read+write (fp64)
+    achieved = flops_b / (launch_ms * 1e-3) / 1e12
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6550.4)
+    traffic = None
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = summ.get(spec.name, {}).get("pass_b_dram_bytes")
+    except Exception:
+        pass
+    total_ms = sum(v[0] for v in prof.values())
+    roofline = {
+        "bound": "tensor", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
+        "frac": achieved / peak64 if peak64 else None, "traffic": traffic,
+        "kernel": "k_pass<B> (g = XᵀZ, logits, online max, Y = X·B; fp64 DMMA)",
+        "peak_source": "fp64 DMMA microkernel measured live (edaa_probe_fp64_peak); "
+                       "MEASURED_PEAKS.json has no fp64 entry",
+        "flops_per_launch": flops_b, "launch_ms": launch_ms,
+        "share_of_step": ms_b / total_ms if total_ms else None,
+        "hbm": {"algorithmic_bytes_per_launch": bytes_b,
+                "achieved_gbs": bytes_b / (launch_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                "frac": bytes_b / (launch_ms * 1e-3) / 1e9 / hbm_peak},
+        "pass_ms": {k: v[0] for k, v in prof.items()},
+    }
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": t_dev / args.steps,
+        "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": (value / PUBLISHED[spec.name]) if spec.name in PUBLISHED and T == 100 else None,
+        "dtype": "f64", "data": "synthetic", "config": workload_config(spec, args),
+        "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(x, spec)
+        except Exception as exc:  # the oracle is absent on this box
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
+                                    "kind": None, "sample": "unavailable: %s" % exc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

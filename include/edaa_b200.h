@@ -120,6 +120,22 @@ typedef void (*edaa_observer_fn)(size_t outer, char block, size_t inner, const d
 EDAA_API int edaa_solve_observed(edaa_ctx* ctx, const edaa_solve_params* params, edaa_observer_fn fn,
                         void* user);
 
+/* Instrumentation.  With profiling on, every pass launch is bracketed by CUDA
+ * events on edaa_stream(); edaa_profile_read returns, per pass kind, the
+ * summed device time (ms) and launch count of the last finished solve
+ * (kind 0 = init pass, 1 = A pass, 2 = B pass, 3 = objective pass).
+ * edaa_launch_count: kernels launched by this context since creation. */
+typedef struct {
+  double ms[4];
+  uint64_t launches[4];
+} edaa_profile;
+EDAA_API int edaa_profile_enable(edaa_ctx* ctx, int on);
+EDAA_API int edaa_profile_read(edaa_ctx* ctx, edaa_profile* out);
+EDAA_API uint64_t edaa_launch_count(const edaa_ctx* ctx);
+/* Measures the fp64 tensor-pipe (DMMA) peak of this device in TFLOP/s with
+ * a register-resident microkernel (the roofline denominator for the passes). */
+EDAA_API int edaa_probe_fp64_peak(edaa_ctx* ctx, double* tflops);
+
 /* Version / capability probe. */
 EDAA_API const char* edaa_version(void);
 EDAA_API size_t edaa_max_endmembers(void);

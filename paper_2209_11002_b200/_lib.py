@@ -36,6 +36,10 @@ class RunRecordC(C.Structure):
                 ("fail_outer", C.c_size_t), ("message", C.c_char * 192)]
 
 
+class ProfileC(C.Structure):
+    _fields_ = [("ms", C.c_double * 4), ("launches", C.c_uint64 * 4)]
+
+
 OBSERVER_FN = C.CFUNCTYPE(None, C.c_size_t, C.c_char, C.c_size_t, C.POINTER(C.c_double),
                           C.POINTER(C.c_double), C.c_size_t, C.c_size_t, C.c_void_p)
 
@@ -58,6 +62,10 @@ SIGNATURES = [
                               C.POINTER(C.c_double)]),
     ("edaa_solve_observed", C.c_int, [C.c_void_p, C.POINTER(SolveParams), OBSERVER_FN,
                                       C.c_void_p]),
+    ("edaa_profile_enable", C.c_int, [C.c_void_p, C.c_int]),
+    ("edaa_profile_read", C.c_int, [C.c_void_p, C.POINTER(ProfileC)]),
+    ("edaa_launch_count", C.c_uint64, [C.c_void_p]),
+    ("edaa_probe_fp64_peak", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("edaa_version", C.c_char_p, []),
     ("edaa_max_endmembers", C.c_size_t, []),
     ("edaa_max_bands", C.c_size_t, []),

@@ -39,9 +39,16 @@ struct edaa_ctx {
     size_t cap = 0;
   };
   Buf A, Lg, Bv, Y, Z, XAt, AAt, Gbuf, colm, colS, collogS, eta_a, eta_b, gamma, trace, part_C,
-      part_m, part_S, part_obj, E, fit, mu, part_fit, seeds, fail_key, fail_code, fail_value, cand,
+      part_m, part_S, part_obj, fac, E, fit, mu, part_fit, seeds, fail_key, fail_code, fail_value, cand,
       selected, fit_min, obsA;
   int fit_blocks = 0;
+  // instrumentation
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_kind;
+  size_t ev_used = 0;
+  edaa_profile last_prof{};
+  uint64_t launches = 0;
   // host copies of the per-run records
   std::vector<double> h_fit, h_mu, h_eta_a, h_eta_b, h_fail_value, h_trace;
   std::vector<int> h_fail_code;
@@ -99,6 +106,23 @@ __global__ void k_pad_copy(const float* src, size_t ld, float* dst, int L, int N
   }
 }
 
+// Register-resident DMMA loop: 4 independent accumulators per lane.
+__global__ void k_dmma_peak(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[4][2];
+  for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+  for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 std::string run_message(int code, size_t outer, double value) {
   char buf[192];
   switch (code) {
@@ -145,12 +169,15 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.nslices = std::min(edaa::kMaxSlices, (d.ntiles + edaa::kTilesPerSlice - 1) / edaa::kTilesPerSlice);
   d.M = static_cast<int>(prm->runs);
   d.p = static_cast<int>(p);
-  d.RC = std::max(1, std::min(32 / d.p, d.M));
+  d.RC = std::max(1, std::min(edaa::kQMax / d.p, d.M));
   d.QCpad = (d.RC * d.p + 7) / 8 * 8;
   d.NCH = (d.M + d.RC - 1) / d.RC;
   d.Qs = d.NCH * d.QCpad;
   d.Lrows = d.Lpad + d.QCpad;
   d.K1 = static_cast<int>(prm->inner_iters_a);
+  d.nbuf = 1;
+  if (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem))
+    return set_err(c, EDAA_ERR_UNSUPPORTED, "tile working set exceeds shared memory");
   *out = d;
   return EDAA_OK;
 }
@@ -180,6 +207,7 @@ int alloc_solve(edaa_ctx* c, const Dims& d, size_t T) {
   EDAA_CUDA(c, ensure(c->part_m, S * d.Qs * 8));
   EDAA_CUDA(c, ensure(c->part_S, S * d.Qs * 8));
   EDAA_CUDA(c, ensure(c->part_obj, S * d.M * 8));
+  EDAA_CUDA(c, ensure(c->fac, S * d.Qs * 8));
   EDAA_CUDA(c, ensure(c->E, static_cast<size_t>(d.M) * d.Lpad * d.p * 8));
   EDAA_CUDA(c, ensure(c->fit, d.M * 8));
   EDAA_CUDA(c, ensure(c->mu, d.M * 8));
@@ -231,6 +259,7 @@ edaa::CombineArgs combine_args(edaa_ctx* c, int t, int mode, int trace_index) {
   a.colm = P<double>(c->colm);
   a.colS = P<double>(c->colS);
   a.collogS = P<double>(c->collogS);
+  a.fac = P<double>(c->fac);
   a.XAt = P<double>(c->XAt);
   a.AAt = P<double>(c->AAt);
   a.trace = P<double>(c->trace);
@@ -257,11 +286,34 @@ edaa::PostArgs post_args(edaa_ctx* c, int mode) {
   return a;
 }
 
-#define EDAA_LAUNCH(ctx, call)                                      \
+#define EDAA_LAUNCH_N(ctx, call, n)                                 \
   do {                                                              \
     cudaError_t e_ = (call);                                        \
     if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #call);      \
+    (ctx)->launches += (n);                                         \
   } while (0)
+#define EDAA_LAUNCH(ctx, call) EDAA_LAUNCH_N(ctx, call, 1)
+
+// A pass launch, bracketed by events when profiling (kind = pass mode).
+int launch_pass_profiled(edaa_ctx* c, int mode, const edaa::PassArgs& pa) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profile) {
+    while (c->ev_pool.size() < 2 * (c->ev_used + 1)) {
+      cudaEvent_t e;
+      EDAA_CUDA(c, cudaEventCreate(&e));
+      c->ev_pool.push_back(e);
+    }
+    e0 = c->ev_pool[2 * c->ev_used];
+    e1 = c->ev_pool[2 * c->ev_used + 1];
+    if (c->ev_kind.size() <= c->ev_used) c->ev_kind.resize(c->ev_used + 1);
+    c->ev_kind[c->ev_used] = mode;
+    ++c->ev_used;
+    EDAA_CUDA(c, cudaEventRecord(e0, c->stream));
+  }
+  EDAA_LAUNCH(c, edaa::launch_pass(mode, pa, c->stream));
+  if (c->profile) EDAA_CUDA(c, cudaEventRecord(e1, c->stream));
+  return EDAA_OK;
+}
 
 // Observer hooks used by edaa_solve_observed (null in the batched path).
 struct ObserveHook {
@@ -310,6 +362,7 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   EDAA_CUDA(c, cudaMemsetAsync(c->Gbuf.p, 0, static_cast<size_t>(d.QCpad) * d.Qs * 8, st));
   EDAA_CUDA(c, cudaMemsetAsync(c->E.p, 0, static_cast<size_t>(d.M) * d.Lpad * d.p * 8, st));
   EDAA_CUDA(c, cudaMemsetAsync(c->Lg.p, 0, static_cast<size_t>(d.M) * d.p * d.Npad * 8, st));
+  c->ev_used = 0;
   k_fill_a<<<592, 256, 0, st>>>(P<double>(c->A), d.M, d.p, d.N, d.Npad);
   EDAA_LAUNCH(c, cudaGetLastError());
 
@@ -322,15 +375,17 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   // ---- initialisation: B⁰, Y⁰ = X·B⁰, η, G ----
   {
     edaa::PassArgs pa = pass_args(c, 0, nullptr);
-    EDAA_LAUNCH(c, edaa::launch_pass(edaa::kModeInit, pa, st));
-    EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, 0, edaa::kModeInit, 0), st));
+    rc = launch_pass_profiled(c, edaa::kModeInit, pa);
+    if (rc) return rc;
+    EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, 0, edaa::kModeInit, 0), st), 2);
     EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostInit), st));
   }
   for (size_t t = 1; t <= c->T; ++t) {
     const int ti = static_cast<int>(t);
     edaa::PassArgs pa = pass_args(c, ti, P<double>(c->Y));
     if (hook) pa.observe_A = P<double>(c->obsA);
-    EDAA_LAUNCH(c, edaa::launch_pass(edaa::kModeA, pa, st));
+    rc = launch_pass_profiled(c, edaa::kModeA, pa);
+    if (rc) return rc;
     EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeA, ti - 1), st));
     EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostZ), st));
     if (hook) {
@@ -351,8 +406,9 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
     }
     for (size_t k = 1; k <= prm->inner_iters_b; ++k) {
       edaa::PassArgs pb = pass_args(c, ti, P<double>(c->Z));
-      EDAA_LAUNCH(c, edaa::launch_pass(edaa::kModeB, pb, st));
-      EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0), st));
+      rc = launch_pass_profiled(c, edaa::kModeB, pb);
+      if (rc) return rc;
+      EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0), st), 2);
       const bool last = (k == prm->inner_iters_b);
       EDAA_LAUNCH(c, edaa::launch_post(post_args(c, last ? edaa::kPostG : edaa::kPostZ), st));
       if (hook) {
@@ -374,14 +430,15 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   // ---- finalisation: trace[T], B̂, Ê = X·B̂, fit, coherence ----
   {
     edaa::PassArgs po = pass_args(c, static_cast<int>(c->T), P<double>(c->Y));
-    EDAA_LAUNCH(c, edaa::launch_pass(edaa::kModeObj, po, st));
+    rc = launch_pass_profiled(c, edaa::kModeObj, po);
+    if (rc) return rc;
     edaa::CombineArgs co = combine_args(c, static_cast<int>(c->T), edaa::kModeObj, static_cast<int>(c->T));
     EDAA_LAUNCH(c, edaa::launch_combine(co, st));
     EDAA_LAUNCH(c, edaa::launch_materialize_b(P<double>(c->Lg), P<double>(c->colm), P<double>(c->colS),
                                               P<double>(c->Bv), d, st));
     EDAA_LAUNCH(c, edaa::launch_strict_e(c->X, P<double>(c->Bv), P<double>(c->E), d, st));
-    EDAA_LAUNCH(c, edaa::launch_fit(c->X, P<double>(c->E), P<double>(c->A), P<double>(c->part_fit),
-                                    P<double>(c->fit), c->fit_blocks, d, st));
+    EDAA_LAUNCH_N(c, edaa::launch_fit(c->X, P<double>(c->E), P<double>(c->A), P<double>(c->part_fit),
+                                    P<double>(c->fit), c->fit_blocks, d, st), 2);
     EDAA_LAUNCH(c, edaa::launch_coherence(P<double>(c->E), P<double>(c->mu), d, st));
   }
   return EDAA_OK;
@@ -420,7 +477,7 @@ int edaa_destroy(edaa_ctx* c) {
   cudaStreamSynchronize(c->stream);
   edaa_ctx::Buf* bufs[] = {&c->A, &c->Lg, &c->Bv, &c->Y, &c->Z, &c->XAt, &c->AAt, &c->Gbuf,
                            &c->colm, &c->colS, &c->collogS, &c->eta_a, &c->eta_b, &c->gamma,
-                           &c->trace, &c->part_C, &c->part_m, &c->part_S, &c->part_obj, &c->E,
+                           &c->trace, &c->part_C, &c->part_m, &c->part_S, &c->part_obj, &c->fac, &c->E,
                            &c->fit, &c->mu, &c->part_fit, &c->seeds, &c->fail_key, &c->fail_code,
                            &c->fail_value, &c->cand, &c->selected, &c->fit_min, &c->obsA};
   for (auto* b : bufs)
@@ -522,7 +579,63 @@ int edaa_finish(edaa_ctx* c) {
   EDAA_CUDA(c, cudaMemcpy(c->h_fail_code.data(), c->fail_code.p, d.M * 4, cudaMemcpyDeviceToHost));
   EDAA_CUDA(c, cudaMemcpy(c->h_fail_key.data(), c->fail_key.p, d.M * 8, cudaMemcpyDeviceToHost));
   EDAA_CUDA(c, cudaMemcpy(c->h_trace.data(), c->trace.p, c->h_trace.size() * 8, cudaMemcpyDeviceToHost));
+  c->last_prof = edaa_profile{};
+  for (size_t i = 0; i < c->ev_used; ++i) {
+    float ms = 0.f;
+    EDAA_CUDA(c, cudaEventElapsedTime(&ms, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]));
+    const int k = c->ev_kind[i];
+    c->last_prof.ms[k] += ms;
+    c->last_prof.launches[k] += 1;
+  }
+  c->ev_used = 0;
   c->solved = true;
+  return EDAA_OK;
+}
+
+int edaa_profile_enable(edaa_ctx* c, int on) {
+  if (!c) return EDAA_ERR_INVALID;
+  c->profile = on != 0;
+  return EDAA_OK;
+}
+
+int edaa_profile_read(edaa_ctx* c, edaa_profile* out) {
+  if (!c || !out) return EDAA_ERR_INVALID;
+  *out = c->last_prof;
+  return EDAA_OK;
+}
+
+uint64_t edaa_launch_count(const edaa_ctx* c) { return c ? c->launches : 0; }
+
+int edaa_probe_fp64_peak(edaa_ctx* c, double* tflops) {
+  if (!c || !tflops) return EDAA_ERR_INVALID;
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  int sms = 0;
+  EDAA_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  double* out = nullptr;
+  EDAA_CUDA(c, cudaMalloc(&out, static_cast<size_t>(sms) * 2 * 256 * 8));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20000;
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, c->stream);
+    k_dmma_peak<<<sms * 2, 256, 0, c->stream>>>(out, rep == 0 ? 100 : iters);
+    cudaEventRecord(e1, c->stream);
+    cudaError_t e = cudaEventSynchronize(e1);
+    if (e != cudaSuccess) {
+      cudaFree(out);
+      return cuda_fail(c, e, "k_dmma_peak");
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flop = 2.0 * 256 * 4 * static_cast<double>(iters) * sms * 2 * 256 / 32;
+    if (rep > 0) best = std::max(best, flop / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  *tflops = best;
   return EDAA_OK;
 }
 

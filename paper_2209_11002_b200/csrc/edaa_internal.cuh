@@ -21,12 +21,14 @@
 
 namespace edaa {
 
-constexpr int kThreads = 256;   // 8 warps per CTA
-constexpr int kNP = 64;         // pixels per tile
-constexpr int kXST = kNP + 8;   // fp32 X tile row stride (bank-conflict free DMMA B-frags)
+constexpr int kThreads = 256;   // 8 warps per CTA, two CTAs per SM
+constexpr int kNP = 32;         // pixels per tile
+constexpr int kXST = kNP + 8;   // fp32 X tile row stride (conflict-free DMMA B-frags)
 constexpr int kSST = kNP + 4;   // fp64 weight tile row stride
+constexpr int kQMax = 24;       // columns per chunk (3 DMMA column tiles)
+constexpr int kMaxCT = kQMax / 8;
 constexpr int kMaxSlices = 296; // 2 × 148 SMs
-constexpr int kTilesPerSlice = 4;
+constexpr int kTilesPerSlice = 8;
 constexpr int kMaxP = 16;
 constexpr int kMaxLpad = 320;
 constexpr double kLogFloorValue = 1e-30;  // solver.cpp:15
@@ -49,6 +51,7 @@ struct Dims {
   int M, p, RC, QCpad, NCH, Qs;
   int Lrows;  // Lpad + QCpad (A-pass pseudo rows carry AAᵀ)
   int K1;
+  int nbuf;   // X tile buffers in shared memory (2 = prefetch next tile)
 };
 
 struct PassArgs {
@@ -85,6 +88,7 @@ struct CombineArgs {
   double* colm;
   double* colS;
   double* collogS;
+  double* fac;      // [nslices][Qs] scratch: exp(m_s − m) per slice and column
   double* XAt;      // A output
   double* AAt;      // A output [QCpad][Qs]
   double* trace;    // [M][T+1]
@@ -126,6 +130,7 @@ cudaError_t launch_select(const double* fit, const double* mu, const int* fail_c
                           const unsigned long long* fail_key, int M, double slack,
                           unsigned char* cand, long long* selected, double* fit_min,
                           cudaStream_t st);
-size_t pass_smem_bytes(int mode, const Dims& d);
+size_t pass_smem_bytes(const Dims& d, int nbuf);
+constexpr int kMaxSmem = 232448;  // sm_100 opt-in dynamic shared memory per block
 
 }  // namespace edaa

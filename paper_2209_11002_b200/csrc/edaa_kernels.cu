@@ -45,9 +45,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // SplitMix64 draw number `index` (0-based) of the stream seeded with `seed`:
 // the state after index+1 increments (prng.hpp:15-26), mapped to [0,1)
@@ -65,134 +64,204 @@ __device__ __forceinline__ double max_like_std(double top, double s) {
 }
 
 struct SmemLayout {
-  int xs_off, ws_off, ss_off, obj_off, gs_off, col_off, total;
+  int xs_off, ws_off, ss_off, sh_off, st_off, gs_off, col_off, total;
 };
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 
+// W row stride (doubles): ≡ 8 mod 16 so a DMMA A-fragment (4 rows × 8 columns) hits 2 wavefronts.
 __host__ __device__ inline int w_stride(int qcpad) { return qcpad + ((qcpad % 16 == 0) ? 8 : 0); }
 
-__host__ __device__ inline SmemLayout smem_layout(const Dims& d) {
+__host__ __device__ inline SmemLayout smem_layout(const Dims& d, int /*nbuf*/) {
   SmemLayout s;
   int off = 0;
-  s.xs_off = off;
+  s.xs_off = off;  // X tile, fp32 [Lpad][kXST]
   off += align16(d.Lpad * kXST * 4);
-  s.ws_off = off;
+  s.ws_off = off;  // W chunk, fp64 [Lpad][WST]
   off += align16(d.Lpad * w_stride(d.QCpad) * 8);
-  s.ss_off = off;
+  s.ss_off = off;  // projection / weights, fp64 [QCpad][kSST]
   off += align16(d.QCpad * kSST * 8);
-  s.obj_off = off;
-  off += align16(d.RC * kNP * 8);
+  s.sh_off = off;  // second half of the band-split projection
+  off += align16(d.QCpad * kSST * 8);
+  s.st_off = off;  // state tile (A or logits) of the chunk, fp64 [QCpad][kNP]
+  off += align16(d.QCpad * kNP * 8);
   s.gs_off = off;
   off += align16(d.RC * d.p * d.p * 8);
-  s.col_off = off;  // m_run, S_run, fac (QCpad each) + obj_run (RC)
-  off += align16((3 * d.QCpad + d.RC) * 8);
+  s.col_off = off;  // m_run, S_run, fac, hmax, hsum (QCpad each) + obj_run (RC), hobj (4·RC)
+  off += align16((5 * d.QCpad + 5 * d.RC) * 8);
   s.total = off;
   return s;
 }
 
-// ---------------------------------------------------------------------------
-// Per-pixel A update: objective term + K1 entropic steps (solver.cpp:212-218).
-// P (= Yᵀx_j, the projection) is read from the weight tile; G = YᵀY of the
-// run is in shared memory; a is the pixel's p-vector.
-// log(a_i) after a softmax is carried in the log domain,
-// log a_i = s_i − top − log Σ, which equals log(e_i/Σ) up to rounding; the
-// 1e-30 floor is applied to it as solver.cpp:25 does to a_i.
-template <int PT, bool UPDATE>
-__device__ __forceinline__ void pixel_a_update(const PassArgs& pa, int r, int rl, int j, int pix,
-                                               double* ss, const double* gs, double* obj_s) {
-  const Dims& d = pa.d;
-  const int p = d.p;
-  double a[PT], la[PT];
-  const size_t base = static_cast<size_t>(r) * p * d.Npad + pix;
+__device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-  for (int i = 0; i < PT; ++i) {
-    if (i < p) {
-      a[i] = pa.A[base + static_cast<size_t>(i) * d.Npad];
-      const double z = (a[i] < kLogFloorValue) ? kLogFloorValue : a[i];  // std::max(z, 1e-30)
-      la[i] = log(z);
-    }
-  }
-  const double* G = gs + rl * p * p;
-  const double* Pcol = ss + (rl * p) * kSST + j;
-  const double eta = pa.eta_a[r];
-  double aPa = 0.0, aGa = 0.0;
-  const int steps = UPDATE ? d.K1 : 1;
-  bool bad = false;
-  for (int k = 0; k < steps; ++k) {
-    double top = -INFINITY;
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      if (i < p) {
-        double ga = 0.0;
-#pragma unroll
-        for (int m = 0; m < PT; ++m)
-          if (m < p) ga += G[i * p + m] * a[m];
-        const double Pi = Pcol[i * kSST];
-        if (k == 0) {
-          aPa += a[i] * Pi;
-          aGa += a[i] * ga;
-        }
-        // −∇_A = (XB)ᵀ(X − XBA) = P − G·a, scaled by η_a, added to log z.
-        const double s = la[i] + (Pi - ga) * eta;
-        la[i] = s;
-        top = max_like_std(top, s);
-      }
-    }
-    if (!UPDATE) break;
-    double total = 0.0;
-#pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      if (i < p) {
-        a[i] = exp(la[i] - top);
-        total += a[i];
-      }
-    }
-    const double ltot = log(total);
-#pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      if (i < p) {
-        a[i] = a[i] / total;
-        bad |= !isfinite(a[i]);
-        const double l2 = la[i] - top - ltot;
-        la[i] = (l2 < log_floor()) ? log_floor() : l2;
-      }
-    }
-    if (pa.observe_A != nullptr) {
-#pragma unroll
-      for (int i = 0; i < PT; ++i)
-        if (i < p) pa.observe_A[(static_cast<size_t>(k) * p + i) * d.Npad + pix] = a[i];
-    }
-  }
-  obj_s[rl * kNP + j] = 0.5 * ((pa.xnorm[pix] - 2.0 * aPa) + aGa);
-  if (UPDATE) {
-    if (bad) atomicMin(pa.fail_key + r, static_cast<unsigned long long>(pa.t) << 1);
-#pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      if (i < p) {
-        pa.A[base + static_cast<size_t>(i) * d.Npad] = a[i];
-        ss[(rl * p + i) * kSST + j] = a[i];
-      }
-    }
-  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
 // ---------------------------------------------------------------------------
-// The pass kernel. grid = (nslices, NCH), block = 256.
-template <int MODE, int PT, int RTW>
-__global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
+// Per-pixel A update: objective term + K1 entropic steps (solver.cpp:212-218),
+// one pixel of one run per group of TPP lanes, each lane owning EPT of the p
+// entries.  P (= Yᵀx_j) is the sum of the two band halves in ss/sh, G = YᵀY
+// of the run and the pixel's current a are in shared memory.
+// The softmax of solver.cpp:20-36, softmax(log max(a, 1e-30) + u) with
+// u = η_a·(P − G·a), is evaluated in the equivalent multiplicative form
+// a_i ← max(a_i,1e-30)·e^{u_i − max u} / Σ — the same shift-invariant
+// quantity (every term ≤ 1, the largest ≥ 1e-30, so it neither overflows
+// nor vanishes) without the logarithms.
+// Returns the pixel's objective term ½‖x_j − Y a_j‖² = ½(‖x_j‖² − 2aᵀP + aᵀGa)
+// for the pre-update a (on the group's sub-0 lane, 0 elsewhere).
+template <int PT>
+struct LanesPerPixel {
+  static constexpr int value = PT <= 4 ? 1 : (PT <= 8 ? 2 : 4);
+};
+
+template <int PT, int TPP, bool UPDATE>
+__device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int rl, int j, int pix,
+                                                 bool valid, int sub, double* ss, const double* sh,
+                                                 const double* st, const double* gs) {
+  constexpr int EPT = (PT + TPP - 1) / TPP;
+  const Dims& d = pa.d;
+  const int p = d.p;
+  const int gbase = (threadIdx.x & 31) - sub;
+  double a[EPT], P[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = sub * EPT + e;
+    a[e] = 0.0;
+    P[e] = 0.0;
+    if (i < p) {
+      const int c = rl * p + i;
+      a[e] = st[c * kNP + j];
+      P[e] = ss[c * kSST + j] + sh[c * kSST + j];
+    }
+  }
+  const double* G = gs + rl * p * p;
+  const double eta = pa.eta_a[r];
+  double aPa = 0.0, aGa = 0.0;
+  bool bad = false;
+  const int steps = UPDATE ? d.K1 : 1;
+  for (int k = 0; k < steps; ++k) {
+    double ga[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) ga[e] = 0.0;
+#pragma unroll
+    for (int m = 0; m < PT; ++m) {
+      if (m < p) {
+        const double am = (TPP == 1) ? a[m % EPT] : __shfl_sync(0xffffffffu, a[m % EPT], gbase + m / EPT);
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const int i = sub * EPT + e;
+          if (i < p) ga[e] += G[i * p + m] * am;
+        }
+      }
+    }
+    double u[EPT];
+    double umax = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      u[e] = -INFINITY;
+      if (sub * EPT + e < p) {
+        if (k == 0) {
+          aPa += a[e] * P[e];
+          aGa += a[e] * ga[e];
+        }
+        u[e] = (P[e] - ga[e]) * eta;  // −∇_A = (XB)ᵀ(X − XBA) = P − G·a, times η_a
+        umax = fmax(umax, u[e]);
+      }
+    }
+    if (!UPDATE) break;
+#pragma unroll
+    for (int o = 1; o < TPP; o <<= 1) umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+    double total = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      if (sub * EPT + e < p) {
+        const double z = (a[e] < kLogFloorValue) ? kLogFloorValue : a[e];  // std::max(z, 1e-30)
+        a[e] = z * exp(u[e] - umax);
+        total += a[e];
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < TPP; o <<= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    const double inv = 1.0 / total;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = sub * EPT + e;
+      if (i < p) {
+        a[e] *= inv;
+        bad |= !isfinite(a[e]);
+        if (pa.observe_A != nullptr && valid)
+          pa.observe_A[(static_cast<size_t>(k) * p + i) * d.Npad + pix] = a[e];
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < TPP; o <<= 1) {
+    aPa += __shfl_xor_sync(0xffffffffu, aPa, o);
+    aGa += __shfl_xor_sync(0xffffffffu, aGa, o);
+  }
+  if (UPDATE) {
+    if (bad && valid) atomicMin(pa.fail_key + r, static_cast<unsigned long long>(pa.t) << 1);
+    const size_t base = static_cast<size_t>(r) * p * d.Npad + pix;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int i = sub * EPT + e;
+      if (i < p) {
+        if (valid) pa.A[base + static_cast<size_t>(i) * d.Npad] = a[e];
+        ss[(rl * p + i) * kSST + j] = valid ? a[e] : 0.0;
+      }
+    }
+  }
+  return (valid && sub == 0) ? 0.5 * ((pa.xnorm[pix] - 2.0 * aPa) + aGa) : 0.0;
+}
+
+// X tile (rows < L) and the chunk's state rows (A or logits) for pixels
+// [j0, j0+kNP), 16-byte cp.async into shared memory, one commit group.
+template <int MODE>
+__device__ __forceinline__ void load_tile(const PassArgs& pa, float* xs, double* st, int j0,
+                                          int state_row0, int nstate) {
+  const Dims& d = pa.d;
+  for (int e = threadIdx.x; e < d.L * (kNP / 4); e += kThreads) {
+    const int l = e / (kNP / 4), q = e % (kNP / 4);
+    cp_async16(xs + l * kXST + q * 4, pa.X + static_cast<size_t>(l) * d.Npad + j0 + q * 4);
+  }
+  if (MODE != kModeInit) {
+    const double* src = (MODE == kModeB) ? pa.Lg : pa.A;
+    for (int e = threadIdx.x; e < nstate * (kNP / 2); e += kThreads) {
+      const int c = e / (kNP / 2), q = e % (kNP / 2);
+      cp_async16(st + c * kNP + q * 2, src + static_cast<size_t>(state_row0 + c) * d.Npad + j0 + q * 2);
+    }
+  }
+  cp_async_commit();
+}
+
+// ---------------------------------------------------------------------------
+// The pass kernel. grid = (nslices, NCH), block = 256, two CTAs per SM so one
+// CTA's per-pixel phase overlaps the other's DMMA phases.
+template <int MODE, int PT, int RTW, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_pass(PassArgs pa) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Dims& d = pa.d;
-  const SmemLayout lay = smem_layout(d);
+  const SmemLayout lay = smem_layout(d, 1);
   float* xs = reinterpret_cast<float*>(smem + lay.xs_off);
   double* ws = reinterpret_cast<double*>(smem + lay.ws_off);
   double* ss = reinterpret_cast<double*>(smem + lay.ss_off);
-  double* obj_s = reinterpret_cast<double*>(smem + lay.obj_off);
+  double* sh = reinterpret_cast<double*>(smem + lay.sh_off);
+  double* st = reinterpret_cast<double*>(smem + lay.st_off);
   double* gs = reinterpret_cast<double*>(smem + lay.gs_off);
   double* m_run = reinterpret_cast<double*>(smem + lay.col_off);
   double* S_run = m_run + d.QCpad;
   double* fac = S_run + d.QCpad;
-  double* obj_run = fac + d.QCpad;
+  double* hmax = fac + d.QCpad;
+  double* hsum = hmax + d.QCpad;
+  double* obj_run = hsum + d.QCpad;
+  double* hobj = obj_run + d.RC;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -208,6 +277,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
   const int nRT = (MODE == kModeA) ? nRTx + d.QCpad / 8 : nRTx;
   const int WST = w_stride(d.QCpad);
   const int col0 = chunk * d.QCpad;
+  const int srow0 = run0 * p;  // first state row (A / Lg) of this chunk
+
+  const int tile_begin = static_cast<int>((static_cast<long long>(slice) * d.ntiles) / d.nslices);
+  const int tile_end = static_cast<int>((static_cast<long long>(slice + 1) * d.ntiles) / d.nslices);
+
+  // first tile in flight while the constants are staged
+  load_tile<MODE>(pa, xs, st, tile_begin * kNP, srow0, ncol_valid);
 
   // ---- one-time staging: W chunk, G blocks, zero pad rows, running state ----
   if (MODE == kModeA || MODE == kModeB || MODE == kModeObj) {
@@ -232,121 +308,124 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
   }
   if (tid < d.RC) obj_run[tid] = 0.0;
 
-  double acc[RTW][4][2];
+  double acc[RTW][kMaxCT][2];
 #pragma unroll
   for (int i = 0; i < RTW; ++i)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
-
-  const int tile_begin = static_cast<int>((static_cast<long long>(slice) * d.ntiles) / d.nslices);
-  const int tile_end = static_cast<int>((static_cast<long long>(slice + 1) * d.ntiles) / d.nslices);
+    for (int c = 0; c < kMaxCT; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
 
   for (int tile = tile_begin; tile < tile_end; ++tile) {
     const int j0 = tile * kNP;
-    // ---- X tile → shared (16 B cp.async, rows < L) ----
-    for (int e = tid; e < d.L * (kNP / 4); e += kThreads) {
-      const int l = e / (kNP / 4), q = e % (kNP / 4);
-      cp_async16(xs + l * kXST + q * 4, pa.X + static_cast<size_t>(l) * d.Npad + j0 + q * 4);
-    }
-    cp_async_wait_all();
+    cp_async_wait0();
     __syncthreads();
 
-    // ---- phase 1: S[c][j] = Σ_l W[l][c]·X[l][j]  (DMMA, warp = 8 pixels) ----
+    // ---- phase 1: S[c][j] = Σ_l W[l][c]·X[l][j]  (DMMA; warp = 8 pixels × one band half) ----
     if (MODE != kModeInit) {
-      double c1[4][2];
+      const int pt = warp & 3, half = warp >> 2;
+      const int kh = d.Lpad / 8;  // k-steps per band half
+      double c1[kMaxCT][2];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) c1[c][0] = c1[c][1] = 0.0;
-      const float* xcol = xs + warp * 8 + g;
+      for (int c = 0; c < kMaxCT; ++c) c1[c][0] = c1[c][1] = 0.0;
+      const float* xcol = xs + pt * 8 + g;
       const double* wcol = ws + g;
-      for (int kk = 0; kk < d.Lpad / 4; ++kk) {
+      for (int kk = half * kh; kk < (half + 1) * kh; ++kk) {
         const int l = kk * 4 + t4;
         const double bx = static_cast<double>(xcol[l * kXST]);
 #pragma unroll
-        for (int ct = 0; ct < 4; ++ct)
+        for (int ct = 0; ct < kMaxCT; ++ct)
           if (ct < nCT) dmma(c1[ct], wcol[l * WST + ct * 8], bx);
       }
+      double* dst = half ? sh : ss;
 #pragma unroll
-      for (int ct = 0; ct < 4; ++ct)
+      for (int ct = 0; ct < kMaxCT; ++ct)
         if (ct < nCT)
-          *reinterpret_cast<double2*>(ss + (ct * 8 + g) * kSST + warp * 8 + 2 * t4) =
+          *reinterpret_cast<double2*>(dst + (ct * 8 + g) * kSST + pt * 8 + 2 * t4) =
               make_double2(c1[ct][0], c1[ct][1]);
     }
     __syncthreads();
 
     // ---- phase 2: per-pixel updates ----
     if (MODE == kModeA || MODE == kModeObj) {
-      for (int q = tid; q < RCe * kNP; q += kThreads) {
+      constexpr int TPP = LanesPerPixel<PT>::value;
+      for (int q2 = tid; q2 < RCe * kNP * TPP; q2 += kThreads) {  // warp-uniform trip count
+        const int q = q2 / TPP, sub = q2 % TPP;
         const int rl = q / kNP, j = q % kNP;
         const int pix = j0 + j;
-        if (pix < d.N) {
-          pixel_a_update<PT, MODE == kModeA>(pa, run0 + rl, rl, j, pix, ss, gs, obj_s);
-        } else {
-          obj_s[rl * kNP + j] = 0.0;
-          if (MODE == kModeA)
-            for (int i = 0; i < p; ++i) ss[(rl * p + i) * kSST + j] = 0.0;
-        }
+        double o = pixel_a_update<PT, TPP, MODE == kModeA>(pa, run0 + rl, rl, j, pix, pix < d.N, sub,
+                                                             ss, sh, st, gs);
+        o = warp_sum(o);
+        if (lane == 0) hobj[q2 >> 5] = o;  // warp-task q2/32 belongs to run (q2/32)/TPP
       }
       if (MODE == kModeA)
         for (int e = tid; e < (d.QCpad - ncol_valid) * kNP; e += kThreads)
           ss[(ncol_valid + e / kNP) * kSST + e % kNP] = 0.0;
       __syncthreads();
-      if (tid < RCe) {  // fixed-order per-run objective partial
-        double s = obj_run[tid];
-        const int jn = min(kNP, d.N - j0);
-        for (int j = 0; j < jn; ++j) s += obj_s[tid * kNP + j];
-        obj_run[tid] = s;
+      if (tid < RCe) {
+        double o = obj_run[tid];
+        for (int h = 0; h < TPP; ++h) o += hobj[tid * TPP + h];
+        obj_run[tid] = o;
       }
       if (MODE == kModeObj) {
         __syncthreads();
+        if (tile + 1 < tile_end) load_tile<MODE>(pa, xs, st, j0 + kNP, srow0, ncol_valid);
         continue;
       }
     } else {  // B step or B⁰ initialisation: new logits, online column max
-      for (int e = tid; e < d.QCpad * kNP; e += kThreads) {
-        const int c = e / kNP, j = e % kNP;
-        const int pix = j0 + j;
-        double ell = -INFINITY;
-        if (c < ncol_valid && pix < d.N) {
-          const int rl = c / p, i = c % p, r = run0 + rl;
-          const size_t idx = (static_cast<size_t>(r) * p + i) * d.Npad + pix;
-          if (MODE == kModeInit) {
-            // solver.cpp:122-127: column i consumes draws i·N .. i·N+N−1.
-            ell = 0.1 * splitmix_unit_at(pa.seeds[r],
-                                         static_cast<uint64_t>(i) * d.N + static_cast<uint64_t>(pix));
-          } else {
-            const int gc = col0 + c;
-            double lb = pa.Lg[idx] - pa.colm[gc] - pa.collogS[gc];  // log b_old
-            lb = (lb < log_floor()) ? log_floor() : lb;              // log max(b, 1e-30)
-            ell = lb + ss[c * kSST + j] * pa.eta_b[r];               // + η_b·(−∇_B)
+      constexpr int kPer = kQMax * kNP / kThreads;  // elements per thread at QCpad = kQMax
+      double ell[kPer];
+      const int per = d.QCpad * kNP / kThreads;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        if (k < per) {
+          const int e = tid + k * kThreads;  // warp = one column × 32 pixels
+          const int c = e / kNP, j = e % kNP;
+          const int pix = j0 + j;
+          double v = -INFINITY;
+          if (c < ncol_valid && pix < d.N) {
+            const int rl = c / p, i = c % p, r = run0 + rl;
+            if (MODE == kModeInit) {
+              // solver.cpp:122-127: column i consumes draws i·N .. i·N+N−1.
+              v = 0.1 * splitmix_unit_at(pa.seeds[r], static_cast<uint64_t>(i) * d.N +
+                                                          static_cast<uint64_t>(pix));
+            } else {
+              const int gc = col0 + c;
+              double lb = st[c * kNP + j] - pa.colm[gc] - pa.collogS[gc];  // log b_old
+              lb = (lb < log_floor()) ? log_floor() : lb;                   // log max(b, 1e-30)
+              v = lb + (ss[c * kSST + j] + sh[c * kSST + j]) * pa.eta_b[r]; // + η_b·(−∇_B)
+            }
+            pa.Lg[static_cast<size_t>(srow0 + c) * d.Npad + pix] = v;
           }
-          pa.Lg[idx] = ell;
+          ell[k] = v;
+          const double hm = warp_max(v);
+          if (lane == 0) hmax[c] = hm;
         }
-        ss[c * kSST + j] = ell;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        if (k < per) {
+          const int e = tid + k * kThreads;
+          const int c = e / kNP, j = e % kNP;
+          const double mn = fmax(m_run[c], hmax[c]);
+          const double w = (mn == -INFINITY) ? 0.0 : exp(ell[k] - mn);
+          ss[c * kSST + j] = w;
+          const double hs = warp_sum(w);
+          if (lane == 0) hsum[c] = hs;
+        }
       }
       __syncthreads();
       if (tid < d.QCpad) {
-        double tmax = -INFINITY;
-        for (int j = 0; j < kNP; ++j) tmax = max_like_std(tmax, ss[tid * kSST + j]);
         const double mo = m_run[tid];
-        const double mn = max_like_std(mo, tmax);
-        fac[tid] = (mn == -INFINITY || mn == mo) ? 1.0 : exp(mo - mn);
+        const double mn = fmax(mo, hmax[tid]);
+        const double f = (mn == -INFINITY || mn == mo) ? 1.0 : exp(mo - mn);
+        fac[tid] = f;
+        S_run[tid] = S_run[tid] * f + hsum[tid];
         m_run[tid] = mn;
       }
       __syncthreads();
-      for (int e = tid; e < d.QCpad * kNP; e += kThreads) {
-        const int c = e / kNP, j = e % kNP;
-        const double m = m_run[c];
-        const double v = ss[c * kSST + j];
-        ss[c * kSST + j] = (m == -INFINITY) ? 0.0 : exp(v - m);
-      }
-      __syncthreads();
-      if (tid < d.QCpad) {
-        double s = S_run[tid] * fac[tid];
-        for (int j = 0; j < kNP; ++j) s += ss[tid * kSST + j];
-        S_run[tid] = s;
-      }
       // rescale running accumulators to the new column max
 #pragma unroll
-      for (int ct = 0; ct < 4; ++ct) {
+      for (int ct = 0; ct < kMaxCT; ++ct) {
         if (ct < nCT) {
           const double f0 = fac[ct * 8 + 2 * t4], f1 = fac[ct * 8 + 2 * t4 + 1];
           if (f0 != 1.0 || f1 != 1.0) {
@@ -363,10 +442,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
     // ---- phase 3: C[l][c] += Σ_j X[l][j]·w[c][j]  (DMMA, warp owns row tiles) ----
     {
       const double* wrow = ss + g * kSST + t4;
+#pragma unroll 2
       for (int kk = 0; kk < kNP / 4; ++kk) {
-        double bw[4];
+        double bw[kMaxCT];
 #pragma unroll
-        for (int ct = 0; ct < 4; ++ct) bw[ct] = (ct < nCT) ? wrow[ct * 8 * kSST + kk * 4] : 0.0;
+        for (int ct = 0; ct < kMaxCT; ++ct) bw[ct] = (ct < nCT) ? wrow[ct * 8 * kSST + kk * 4] : 0.0;
 #pragma unroll
         for (int i = 0; i < RTW; ++i) {
           const int rt = warp + 8 * i;
@@ -377,13 +457,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
             else
               ax = ss[((rt - nRTx) * 8 + g) * kSST + kk * 4 + t4];
 #pragma unroll
-            for (int ct = 0; ct < 4; ++ct)
+            for (int ct = 0; ct < kMaxCT; ++ct)
               if (ct < nCT) dmma(acc[i][ct], ax, bw[ct]);
           }
         }
       }
     }
     __syncthreads();
+    if (tile + 1 < tile_end) load_tile<MODE>(pa, xs, st, j0 + kNP, srow0, ncol_valid);
   }
 
   // ---- write this CTA's partials ----
@@ -394,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
       if (rt < nRT) {
         const int row = rt * 8 + g;
 #pragma unroll
-        for (int ct = 0; ct < 4; ++ct) {
+        for (int ct = 0; ct < kMaxCT; ++ct) {
           if (ct < nCT) {
             double* dst = pa.part_C + (static_cast<size_t>(slice) * d.Lrows + row) * d.Qs + col0 +
                           ct * 8 + 2 * t4;
@@ -415,69 +496,66 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
 }
 
 // ---------------------------------------------------------------------------
-// Combine: block = 256 threads over 32 columns × 8 row lanes.
-__global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// Combine, B/init: per column the log-sum-exp merge of the slice partials,
+// m = max_s m_s, S = Σ_s S_s·e^{m_s − m}; one warp per column, lanes stride
+// the slices, fixed xor-tree merge (deterministic).
+__global__ void k_colnorm(CombineArgs ca) {
   const Dims& d = ca.d;
-  const int lane = threadIdx.x & 31, ry = threadIdx.x >> 5;
-  const int col = blockIdx.x * 32 + lane;
-  const bool colv = col < d.Qs;
+  const int col = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (col >= d.Qs) return;
   const int S = d.nslices;
-  if (ca.mode == kModeA || ca.mode == kModeObj) {
-    for (int row = ry; ca.mode == kModeA && row < d.Lrows; row += 8) {
-      if (!colv) continue;
-      double s = 0.0;
-      for (int sl = 0; sl < S; ++sl) s += ca.part_C[(static_cast<size_t>(sl) * d.Lrows + row) * d.Qs + col];
-      if (row < d.Lpad)
-        ca.XAt[static_cast<size_t>(row) * d.Qs + col] = s;
-      else
-        ca.AAt[static_cast<size_t>(row - d.Lpad) * d.Qs + col] = s;
-    }
-    if (blockIdx.x == 0) {
-      for (int r = threadIdx.x; r < d.M; r += blockDim.x) {
-        double o = 0.0;
-        for (int sl = 0; sl < S; ++sl) o += ca.part_obj[static_cast<size_t>(sl) * d.M + r];
-        ca.trace[static_cast<size_t>(r) * ca.trace_stride + ca.trace_index] = o;
-      }
-    }
-    return;
+  double m = -INFINITY;
+  for (int sl = lane; sl < S; sl += 32) m = fmax(m, ca.part_m[static_cast<size_t>(sl) * d.Qs + col]);
+  m = warp_max(m);
+  double Ssum = 0.0;
+  for (int sl = lane; sl < S; sl += 32) {
+    const double ms = ca.part_m[static_cast<size_t>(sl) * d.Qs + col];
+    const double f = (ms == -INFINITY) ? 0.0 : exp(ms - m);
+    ca.fac[static_cast<size_t>(sl) * d.Qs + col] = f;
+    Ssum += ca.part_S[static_cast<size_t>(sl) * d.Qs + col] * f;
   }
-  // log-sum-exp combine of the per-slice column softmax partials
-  double* fs = reinterpret_cast<double*>(smem);  // [S][32]
-  __shared__ double Ssh[32];
-  if (ry == 0) {
-    double m = -INFINITY, Ssum = 0.0;
-    if (colv) {
-      for (int sl = 0; sl < S; ++sl) m = max_like_std(m, ca.part_m[static_cast<size_t>(sl) * d.Qs + col]);
-      for (int sl = 0; sl < S; ++sl) {
-        const double ms = ca.part_m[static_cast<size_t>(sl) * d.Qs + col];
-        const double f = (ms == -INFINITY) ? 0.0 : exp(ms - m);
-        fs[sl * 32 + lane] = f;
-        Ssum += ca.part_S[static_cast<size_t>(sl) * d.Qs + col] * f;
-      }
-      ca.colm[col] = m;
-      ca.colS[col] = Ssum;
-      ca.collogS[col] = log(Ssum);
-      // A B column is valid iff it belongs to a run; padded slots have m = −inf.
-      const int chunk = col / d.QCpad, c = col % d.QCpad;
-      const int r = chunk * d.RC + c / d.p;
-      if (c < d.RC * d.p && r < d.M && m != -INFINITY) {
-        if (!(isfinite(m) && isfinite(Ssum) && Ssum > 0.0))
-          atomicMin(ca.fail_key + r, (static_cast<unsigned long long>(ca.t) << 1) | 1ull);
-      } else if (c < d.RC * d.p && r < d.M) {
-        atomicMin(ca.fail_key + r, (static_cast<unsigned long long>(ca.t) << 1) | 1ull);
-      }
+  Ssum = warp_sum(Ssum);
+  if (lane != 0) return;
+  ca.colm[col] = m;
+  ca.colS[col] = Ssum;
+  ca.collogS[col] = log(Ssum);
+  // A column of a real run must have a finite max and a finite positive sum.
+  const int chunk = col / d.QCpad, c = col % d.QCpad;
+  const int r = chunk * d.RC + c / d.p;
+  if (c < d.RC * d.p && r < d.M && !(isfinite(m) && isfinite(Ssum) && Ssum > 0.0))
+    atomicMin(ca.fail_key + r, (static_cast<unsigned long long>(ca.t) << 1) | 1ull);
+}
+
+// Row sums over slices (fixed order): A mode → XAt / AAt; B/init → Y = Σ C_s·fac_s / S.
+// Block (32 columns × 8 rows); block (0,0) also folds the per-run objective.
+__global__ void k_rowsum(CombineArgs ca, int rows) {
+  const Dims& d = ca.d;
+  const int col = blockIdx.x * 32 + threadIdx.x;
+  const int row = blockIdx.y * 8 + threadIdx.y;
+  const int S = d.nslices;
+  if ((ca.mode == kModeA || ca.mode == kModeObj) && blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int r = threadIdx.y * 32 + threadIdx.x; r < d.M; r += 256) {
+      double o = 0.0;
+      for (int sl = 0; sl < S; ++sl) o += ca.part_obj[static_cast<size_t>(sl) * d.M + r];
+      ca.trace[static_cast<size_t>(r) * ca.trace_stride + ca.trace_index] = o;
     }
-    Ssh[lane] = Ssum;
   }
-  __syncthreads();
-  if (!colv) return;
-  const double Ssum = Ssh[lane];
-  for (int row = ry; row < d.Lpad; row += 8) {
-    double s = 0.0;
-    for (int sl = 0; sl < S; ++sl)
-      s += ca.part_C[(static_cast<size_t>(sl) * d.Lrows + row) * d.Qs + col] * fs[sl * 32 + lane];
-    ca.Y[static_cast<size_t>(row) * d.Qs + col] = s / Ssum;
+  if (col >= d.Qs || row >= rows) return;
+  const double* src = ca.part_C + static_cast<size_t>(row) * d.Qs + col;
+  const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
+  double s = 0.0;
+  if (ca.mode == kModeA) {
+#pragma unroll 8
+    for (int sl = 0; sl < S; ++sl) s += src[sl * sstride];
+    if (row < d.Lpad)
+      ca.XAt[static_cast<size_t>(row) * d.Qs + col] = s;
+    else
+      ca.AAt[static_cast<size_t>(row - d.Lpad) * d.Qs + col] = s;
+  } else {
+#pragma unroll 8
+    for (int sl = 0; sl < S; ++sl) s += src[sl * sstride] * ca.fac[static_cast<size_t>(sl) * d.Qs + col];
+    ca.Y[static_cast<size_t>(row) * d.Qs + col] = s / ca.colS[col];
   }
 }
 
@@ -719,16 +797,17 @@ __global__ void k_select(const double* fit, const double* mu, const int* fail_co
 
 template <int MODE, int RTW>
 cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
+  constexpr int MB = (RTW <= 4) ? 2 : 1;
   const dim3 grid(a.d.nslices, a.d.NCH);
-  const size_t smem = smem_layout(a.d).total;
+  const size_t smem = smem_layout(a.d, a.d.nbuf).total;
   void (*kern)(PassArgs) = nullptr;
   if (MODE == kModeInit || MODE == kModeB) {
-    kern = k_pass<MODE, 1, RTW>;
+    kern = k_pass<MODE, 1, RTW, MB>;
   } else {
     switch (pt) {
-#define EDAA_PT_CASE(P) \
-  case P:               \
-    kern = k_pass<MODE, P, RTW>; \
+#define EDAA_PT_CASE(P)                                       \
+  case P:                                                     \
+    kern = k_pass<MODE, P, RTW, (P <= 12 ? MB : 1)>;          \
     break;
       EDAA_PT_CASE(2) EDAA_PT_CASE(3) EDAA_PT_CASE(4) EDAA_PT_CASE(5) EDAA_PT_CASE(6)
       EDAA_PT_CASE(7) EDAA_PT_CASE(8) EDAA_PT_CASE(10) EDAA_PT_CASE(12) EDAA_PT_CASE(16)
@@ -753,11 +832,11 @@ int pt_bucket(int p) {
 
 }  // namespace
 
-size_t pass_smem_bytes(int /*mode*/, const Dims& d) { return smem_layout(d).total; }
+size_t pass_smem_bytes(const Dims& d, int nbuf) { return smem_layout(d, nbuf).total; }
 
 cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st) {
   const int pt = pt_bucket(a.d.p);
-  const bool wide = (a.d.Lpad / 8 + a.d.QCpad / 8) > 32;
+  const bool wide = (a.d.Lpad / 8 + a.d.QCpad / 8) > 32;  // > 4 row tiles per warp
   switch (mode) {
     case kModeInit:
       return wide ? launch_pass_rtw<kModeInit, 6>(a, st, pt) : launch_pass_rtw<kModeInit, 4>(a, st, pt);
@@ -772,12 +851,15 @@ cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
-  const int blocks = (a.d.Qs + 31) / 32;
-  const size_t smem = (a.mode == kModeA || a.mode == kModeObj) ? 0 : static_cast<size_t>(a.d.nslices) * 32 * 8;
-  cudaError_t e = cudaFuncSetAttribute(k_combine, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  k_combine<<<blocks, 256, smem, st>>>(a);
+  const Dims& d = a.d;
+  if (a.mode == kModeB || a.mode == kModeInit) {
+    k_colnorm<<<(d.Qs + 7) / 8, 256, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const int rows = (a.mode == kModeA) ? d.Lrows : (a.mode == kModeObj ? 0 : d.Lpad);
+  const dim3 grid((d.Qs + 31) / 32, rows > 0 ? (rows + 7) / 8 : 1);
+  k_rowsum<<<grid, dim3(32, 8), 0, st>>>(a, rows);
   return cudaGetLastError();
 }
 

@@ -257,6 +257,24 @@ class Device:
         self._check(self.lib.edaa_solve_observed(self.h, C.byref(prm), fn, None))
         del N
 
+    # -- instrumentation ---------------------------------------------------------
+    def profile_enable(self, on: bool = True):
+        self._check(self.lib.edaa_profile_enable(self.h, int(on)))
+
+    def profile(self):
+        """Per pass kind (init, A, B, obj): (summed device ms, launches) of the last solve."""
+        pr = _lib.ProfileC()
+        self._check(self.lib.edaa_profile_read(self.h, C.byref(pr)))
+        return {k: (pr.ms[i], int(pr.launches[i])) for i, k in enumerate(("init", "A", "B", "obj"))}
+
+    def launch_count(self) -> int:
+        return int(self.lib.edaa_launch_count(self.h))
+
+    def fp64_peak_tflops(self) -> float:
+        out = C.c_double()
+        self._check(self.lib.edaa_probe_fp64_peak(self.h, C.byref(out)))
+        return out.value
+
     # -- results ----------------------------------------------------------------
     def record(self, run: int) -> RunRecordC:
         out = RunRecordC()
