@@ -22,8 +22,8 @@
  * Threading: one context per device; a context is not thread-safe (the
  * C++ layer serialises).  All device memory is owned by the context.
  *
- * Precision contract: X is stored as fp32 (callers round once); every
- * contraction with X, every per-pixel update and every reduction is fp64.
+ * Precision contract: X is stored as fp32 (or fp64 via edaa_set_image_host_f64);
+ * every contraction with X, every per-pixel update and every reduction is fp64.
  */
 #ifndef EDAA_B200_H
 #define EDAA_B200_H
@@ -90,10 +90,14 @@ EDAA_API const char* edaa_last_error(const edaa_ctx* ctx);
 /* The cudaStream_t all work is enqueued on (as void*), for event timing. */
 EDAA_API void* edaa_stream(edaa_ctx* ctx);
 
-/* Image X (L×N row-major fp32, bands × pixels, already ℓ2-normalised and
+/* Image X (L×N row-major, bands × pixels, already ℓ2-normalised and
  * validated by the caller).  _host copies from host memory (pinned or
- * pageable); _device copies from a device pointer with row pitch ld (floats). */
+ * pageable); _device copies from a device pointer with row pitch ld (floats).
+ * _host_f64 keeps X in fp64 on the device (for inputs that are not exactly
+ * representable in fp32: results then track the reference on ANY fp64 input;
+ * one CTA per SM instead of two). */
 EDAA_API int edaa_set_image_host(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels);
+EDAA_API int edaa_set_image_host_f64(edaa_ctx* ctx, const double* x, size_t bands, size_t pixels);
 EDAA_API int edaa_set_image_device(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels, size_t ld);
 
 /* Batched Algorithm 1 over all runs.  _async only enqueues on edaa_stream();

@@ -50,6 +50,7 @@ SIGNATURES = [
     ("edaa_last_error", C.c_char_p, [C.c_void_p]),
     ("edaa_stream", C.c_void_p, [C.c_void_p]),
     ("edaa_set_image_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t]),
+    ("edaa_set_image_host_f64", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t]),
     ("edaa_set_image_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
                                         C.c_size_t]),
     ("edaa_solve_async", C.c_int, [C.c_void_p, C.POINTER(SolveParams)]),

@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                   "-I" + os.path.join(ROOT, "include")]
-CUDA_SRCS = ["edaa_kernels.cu", "edaa_capi.cu"]
+CUDA_SRCS = ["edaa_pass_f32.cu", "edaa_pass_f64.cu", "edaa_kernels.cu", "edaa_capi.cu"]
 HOST_SRCS = ["matrix.cpp", "image.cpp", "types.cpp", "solver.cpp", "ensemble.cpp", "device.cpp"]
 
 CUDA_LIB = os.path.join(PKG, "libedaa_cuda.so")
@@ -47,7 +47,7 @@ def _stale(target, deps):
 
 def build_cuda(force=False, verbose=False):
     os.makedirs(BUILD, exist_ok=True)
-    hdrs = [os.path.join(CSRC, "edaa_internal.cuh"), os.path.join(ROOT, "include", "edaa_b200.h")]
+    hdrs = [os.path.join(CSRC, h) for h in ("edaa_internal.cuh", "edaa_device.cuh", "edaa_pass.cuh")] + [os.path.join(ROOT, "include", "edaa_b200.h")]
     objs = []
     jobs = []
     for s in CUDA_SRCS:

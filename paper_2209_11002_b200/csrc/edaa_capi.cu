@@ -26,7 +26,8 @@ struct edaa_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   // image
-  float* X = nullptr;
+  void* X = nullptr;  // float or double [L][Npad]
+  int xbytes = 4;
   double* xnorm = nullptr;
   int L = 0, N = 0, Npad = 0;
   size_t x_cap = 0, xn_cap = 0;
@@ -97,12 +98,13 @@ __global__ void k_fill_a(double* A, int M, int p, int N, int Npad) {
   }
 }
 
-__global__ void k_pad_copy(const float* src, size_t ld, float* dst, int L, int N, int Npad) {
+template <class XT>
+__global__ void k_pad_copy(const XT* src, size_t ld, XT* dst, int L, int N, int Npad) {
   const size_t total = static_cast<size_t>(L) * Npad;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const int l = static_cast<int>(i / Npad), j = static_cast<int>(i % Npad);
-    dst[i] = (j < N) ? src[static_cast<size_t>(l) * ld + j] : 0.0f;
+    dst[i] = (j < N) ? src[static_cast<size_t>(l) * ld + j] : XT(0);
   }
 }
 
@@ -160,6 +162,7 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
       return set_err(c, EDAA_ERR_INVALID, "solver config: step factor gamma must be positive");
   Dims d{};
   d.L = c->L;
+  d.xbytes = c->xbytes;
   d.Lpad = (c->L + 7) / 8 * 8;
   if (d.Lpad > edaa::kMaxLpad)
     return set_err(c, EDAA_ERR_UNSUPPORTED, "band count above the compiled maximum (320)");
@@ -493,7 +496,7 @@ const char* edaa_last_error(const edaa_ctx* c) { return c ? c->err.c_str() : "nu
 
 void* edaa_stream(edaa_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
-static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels) {
+static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels, int xbytes) {
   if (bands < 1 || pixels < 1)
     return set_err(c, EDAA_ERR_INVALID, "image: needs at least one band and one pixel");
   if (pixels > (1u << 30) || bands > (1u << 20)) return set_err(c, EDAA_ERR_UNSUPPORTED, "image too large");
@@ -501,7 +504,8 @@ static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels) {
   c->L = static_cast<int>(bands);
   c->N = static_cast<int>(pixels);
   c->Npad = (c->N + edaa::kNP - 1) / edaa::kNP * edaa::kNP;
-  const size_t xb = static_cast<size_t>(c->L) * c->Npad * 4;
+  c->xbytes = xbytes;
+  const size_t xb = static_cast<size_t>(c->L) * c->Npad * xbytes;
   if (c->x_cap < xb) {
     if (c->X) cudaFree(c->X);
     c->X = nullptr;
@@ -521,34 +525,45 @@ static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels) {
   return EDAA_OK;
 }
 
-int edaa_set_image_host(edaa_ctx* c, const float* x, size_t bands, size_t pixels) {
+static int upload_host(edaa_ctx* c, const void* x, size_t bands, size_t pixels, int xbytes) {
   if (!c || !x) return set_err(c, EDAA_ERR_INVALID, "null argument");
-  int rc = prepare_image(c, bands, pixels);
+  int rc = prepare_image(c, bands, pixels, xbytes);
   if (rc) return rc;
-  EDAA_CUDA(c, cudaMemcpy2DAsync(c->X, static_cast<size_t>(c->Npad) * 4, x, pixels * 4, pixels * 4,
-                                 bands, cudaMemcpyHostToDevice, c->stream));
+  const size_t pitch = static_cast<size_t>(c->Npad) * xbytes;
+  EDAA_CUDA(c, cudaMemcpy2DAsync(c->X, pitch, x, pixels * xbytes, pixels * xbytes, bands,
+                                 cudaMemcpyHostToDevice, c->stream));
   if (c->Npad > c->N)
-    EDAA_CUDA(c, cudaMemset2DAsync(c->X + c->N, static_cast<size_t>(c->Npad) * 4, 0,
-                                   static_cast<size_t>(c->Npad - c->N) * 4, bands, c->stream));
+    EDAA_CUDA(c, cudaMemset2DAsync(static_cast<char*>(c->X) + pixels * xbytes, pitch, 0,
+                                   static_cast<size_t>(c->Npad - c->N) * xbytes, bands, c->stream));
   Dims d{};
   d.L = c->L;
   d.N = c->N;
   d.Npad = c->Npad;
+  d.xbytes = xbytes;
   EDAA_LAUNCH(c, edaa::launch_xnorm(c->X, c->xnorm, d, c->stream));
   return EDAA_OK;
+}
+
+int edaa_set_image_host(edaa_ctx* c, const float* x, size_t bands, size_t pixels) {
+  return upload_host(c, x, bands, pixels, 4);
+}
+
+int edaa_set_image_host_f64(edaa_ctx* c, const double* x, size_t bands, size_t pixels) {
+  return upload_host(c, x, bands, pixels, 8);
 }
 
 int edaa_set_image_device(edaa_ctx* c, const float* x, size_t bands, size_t pixels, size_t ld) {
   if (!c || !x) return set_err(c, EDAA_ERR_INVALID, "null argument");
   if (ld < pixels) return set_err(c, EDAA_ERR_INVALID, "row pitch smaller than the pixel count");
-  int rc = prepare_image(c, bands, pixels);
+  int rc = prepare_image(c, bands, pixels, 4);
   if (rc) return rc;
-  k_pad_copy<<<592, 256, 0, c->stream>>>(x, ld, c->X, c->L, c->N, c->Npad);
+  k_pad_copy<<<592, 256, 0, c->stream>>>(x, ld, static_cast<float*>(c->X), c->L, c->N, c->Npad);
   EDAA_LAUNCH(c, cudaGetLastError());
   Dims d{};
   d.L = c->L;
   d.N = c->N;
   d.Npad = c->Npad;
+  d.xbytes = 4;
   EDAA_LAUNCH(c, edaa::launch_xnorm(c->X, c->xnorm, d, c->stream));
   return EDAA_OK;
 }

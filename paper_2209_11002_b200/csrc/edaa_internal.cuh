@@ -52,12 +52,13 @@ struct Dims {
   int Lrows;  // Lpad + QCpad (A-pass pseudo rows carry AAᵀ)
   int K1;
   int nbuf;   // X tile buffers in shared memory (2 = prefetch next tile)
+  int xbytes; // 4: fp32 image, 8: fp64 image (inputs not exactly representable in fp32)
 };
 
 struct PassArgs {
   Dims d;
   int t;  // outer iteration (1-based); 0 for init
-  const float* X;
+  const void* X;          // float or double [L][Npad] (Dims::xbytes)
   const double* xnorm;
   const double* W;        // Y (A/OBJ pass) or Z (B pass), [Lpad][Qs]
   double* A;              // [M][p][Npad]
@@ -118,12 +119,12 @@ struct PostArgs {
 cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st);
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 cudaError_t launch_post(const PostArgs& a, cudaStream_t st);
-cudaError_t launch_xnorm(const float* X, double* xnorm, const Dims& d, cudaStream_t st);
+cudaError_t launch_xnorm(const void* X, double* xnorm, const Dims& d, cudaStream_t st);
 cudaError_t launch_materialize_b(const double* Lg, const double* colm, const double* colS,
                                  double* Bv, const Dims& d, cudaStream_t st);
-cudaError_t launch_strict_e(const float* X, const double* Bv, double* E, const Dims& d,
+cudaError_t launch_strict_e(const void* X, const double* Bv, double* E, const Dims& d,
                             cudaStream_t st);
-cudaError_t launch_fit(const float* X, const double* E, const double* A, double* part_fit,
+cudaError_t launch_fit(const void* X, const double* E, const double* A, double* part_fit,
                        double* fit, int fit_blocks, const Dims& d, cudaStream_t st);
 cudaError_t launch_coherence(const double* E, double* mu, const Dims& d, cudaStream_t st);
 cudaError_t launch_select(const double* fit, const double* mu, const int* fail_code,

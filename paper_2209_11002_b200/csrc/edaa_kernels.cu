@@ -22,482 +22,18 @@
 //   B⁰ initialisation  solver.cpp:118-136 (SplitMix64 draw i·N+j, softmax(0.1u))
 //   step sizes         solver.cpp:138-149, matrix.cpp:150-190
 //   fit / coherence    ensemble.cpp:29-60; selection ensemble.cpp:71-94
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
-#include "edaa_internal.cuh"
+#include "edaa_device.cuh"
 
 namespace edaa {
 
 namespace {
 
-__device__ __forceinline__ double log_floor() { return -69.07755278982137; }  // log(1e-30)
+using namespace dev;
 
-// D = A·B + D for one 8×8×4 fp64 tile. Lane (g = lane>>2, t = lane&3) holds
-// A[g][t], B[t][g] and D[g][2t], D[g][2t+1].
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(d[0]), "+d"(d[1])
-      : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-// SplitMix64 draw number `index` (0-based) of the stream seeded with `seed`:
-// the state after index+1 increments (prng.hpp:15-26), mapped to [0,1)
-// with the top 53 bits (prng.hpp:24-26).
-__device__ __forceinline__ double splitmix_unit_at(uint64_t seed, uint64_t index) {
-  uint64_t z = seed + (index + 1ull) * 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  z = z ^ (z >> 31);
-  return static_cast<double>(z >> 11) * 0x1.0p-53;
-}
-
-__device__ __forceinline__ double max_like_std(double top, double s) {
-  return (top < s) ? s : top;  // std::max(top, s): NaN in s is ignored
-}
-
-struct SmemLayout {
-  int xs_off, ws_off, ss_off, sh_off, st_off, gs_off, col_off, total;
-};
-
-__host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
-
-// W row stride (doubles): ≡ 8 mod 16 so a DMMA A-fragment (4 rows × 8 columns) hits 2 wavefronts.
-__host__ __device__ inline int w_stride(int qcpad) { return qcpad + ((qcpad % 16 == 0) ? 8 : 0); }
-
-__host__ __device__ inline SmemLayout smem_layout(const Dims& d, int /*nbuf*/) {
-  SmemLayout s;
-  int off = 0;
-  s.xs_off = off;  // X tile, fp32 [Lpad][kXST]
-  off += align16(d.Lpad * kXST * 4);
-  s.ws_off = off;  // W chunk, fp64 [Lpad][WST]
-  off += align16(d.Lpad * w_stride(d.QCpad) * 8);
-  s.ss_off = off;  // projection / weights, fp64 [QCpad][kSST]
-  off += align16(d.QCpad * kSST * 8);
-  s.sh_off = off;  // second half of the band-split projection
-  off += align16(d.QCpad * kSST * 8);
-  s.st_off = off;  // state tile (A or logits) of the chunk, fp64 [QCpad][kNP]
-  off += align16(d.QCpad * kNP * 8);
-  s.gs_off = off;
-  off += align16(d.RC * d.p * d.p * 8);
-  s.col_off = off;  // m_run, S_run, fac, hmax, hsum (QCpad each) + obj_run (RC), hobj (4·RC)
-  off += align16((5 * d.QCpad + 5 * d.RC) * 8);
-  s.total = off;
-  return s;
-}
-
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// ---------------------------------------------------------------------------
-// Per-pixel A update: objective term + K1 entropic steps (solver.cpp:212-218),
-// one pixel of one run per group of TPP lanes, each lane owning EPT of the p
-// entries.  P (= Yᵀx_j) is the sum of the two band halves in ss/sh, G = YᵀY
-// of the run and the pixel's current a are in shared memory.
-// The softmax of solver.cpp:20-36, softmax(log max(a, 1e-30) + u) with
-// u = η_a·(P − G·a), is evaluated in the equivalent multiplicative form
-// a_i ← max(a_i,1e-30)·e^{u_i − max u} / Σ — the same shift-invariant
-// quantity (every term ≤ 1, the largest ≥ 1e-30, so it neither overflows
-// nor vanishes) without the logarithms.
-// Returns the pixel's objective term ½‖x_j − Y a_j‖² = ½(‖x_j‖² − 2aᵀP + aᵀGa)
-// for the pre-update a (on the group's sub-0 lane, 0 elsewhere).
-template <int PT>
-struct LanesPerPixel {
-  static constexpr int value = PT <= 4 ? 1 : (PT <= 8 ? 2 : 4);
-};
-
-template <int PT, int TPP, bool UPDATE>
-__device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int rl, int j, int pix,
-                                                 bool valid, int sub, double* ss, const double* sh,
-                                                 const double* st, const double* gs) {
-  constexpr int EPT = (PT + TPP - 1) / TPP;
-  const Dims& d = pa.d;
-  const int p = d.p;
-  const int gbase = (threadIdx.x & 31) - sub;
-  double a[EPT], P[EPT];
-#pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    const int i = sub * EPT + e;
-    a[e] = 0.0;
-    P[e] = 0.0;
-    if (i < p) {
-      const int c = rl * p + i;
-      a[e] = st[c * kNP + j];
-      P[e] = ss[c * kSST + j] + sh[c * kSST + j];
-    }
-  }
-  const double* G = gs + rl * p * p;
-  const double eta = pa.eta_a[r];
-  double aPa = 0.0, aGa = 0.0;
-  bool bad = false;
-  const int steps = UPDATE ? d.K1 : 1;
-  for (int k = 0; k < steps; ++k) {
-    double ga[EPT];
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) ga[e] = 0.0;
-#pragma unroll
-    for (int m = 0; m < PT; ++m) {
-      if (m < p) {
-        const double am = (TPP == 1) ? a[m % EPT] : __shfl_sync(0xffffffffu, a[m % EPT], gbase + m / EPT);
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-          const int i = sub * EPT + e;
-          if (i < p) ga[e] += G[i * p + m] * am;
-        }
-      }
-    }
-    double u[EPT];
-    double umax = -INFINITY;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      u[e] = -INFINITY;
-      if (sub * EPT + e < p) {
-        if (k == 0) {
-          aPa += a[e] * P[e];
-          aGa += a[e] * ga[e];
-        }
-        u[e] = (P[e] - ga[e]) * eta;  // −∇_A = (XB)ᵀ(X − XBA) = P − G·a, times η_a
-        umax = fmax(umax, u[e]);
-      }
-    }
-    if (!UPDATE) break;
-#pragma unroll
-    for (int o = 1; o < TPP; o <<= 1) umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
-    double total = 0.0;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      if (sub * EPT + e < p) {
-        const double z = (a[e] < kLogFloorValue) ? kLogFloorValue : a[e];  // std::max(z, 1e-30)
-        a[e] = z * exp(u[e] - umax);
-        total += a[e];
-      }
-    }
-#pragma unroll
-    for (int o = 1; o < TPP; o <<= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-    const double inv = 1.0 / total;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int i = sub * EPT + e;
-      if (i < p) {
-        a[e] *= inv;
-        bad |= !isfinite(a[e]);
-        if (pa.observe_A != nullptr && valid)
-          pa.observe_A[(static_cast<size_t>(k) * p + i) * d.Npad + pix] = a[e];
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 1; o < TPP; o <<= 1) {
-    aPa += __shfl_xor_sync(0xffffffffu, aPa, o);
-    aGa += __shfl_xor_sync(0xffffffffu, aGa, o);
-  }
-  if (UPDATE) {
-    if (bad && valid) atomicMin(pa.fail_key + r, static_cast<unsigned long long>(pa.t) << 1);
-    const size_t base = static_cast<size_t>(r) * p * d.Npad + pix;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int i = sub * EPT + e;
-      if (i < p) {
-        if (valid) pa.A[base + static_cast<size_t>(i) * d.Npad] = a[e];
-        ss[(rl * p + i) * kSST + j] = valid ? a[e] : 0.0;
-      }
-    }
-  }
-  return (valid && sub == 0) ? 0.5 * ((pa.xnorm[pix] - 2.0 * aPa) + aGa) : 0.0;
-}
-
-// X tile (rows < L) and the chunk's state rows (A or logits) for pixels
-// [j0, j0+kNP), 16-byte cp.async into shared memory, one commit group.
-template <int MODE>
-__device__ __forceinline__ void load_tile(const PassArgs& pa, float* xs, double* st, int j0,
-                                          int state_row0, int nstate) {
-  const Dims& d = pa.d;
-  for (int e = threadIdx.x; e < d.L * (kNP / 4); e += kThreads) {
-    const int l = e / (kNP / 4), q = e % (kNP / 4);
-    cp_async16(xs + l * kXST + q * 4, pa.X + static_cast<size_t>(l) * d.Npad + j0 + q * 4);
-  }
-  if (MODE != kModeInit) {
-    const double* src = (MODE == kModeB) ? pa.Lg : pa.A;
-    for (int e = threadIdx.x; e < nstate * (kNP / 2); e += kThreads) {
-      const int c = e / (kNP / 2), q = e % (kNP / 2);
-      cp_async16(st + c * kNP + q * 2, src + static_cast<size_t>(state_row0 + c) * d.Npad + j0 + q * 2);
-    }
-  }
-  cp_async_commit();
-}
-
-// ---------------------------------------------------------------------------
-// The pass kernel. grid = (nslices, NCH), block = 256, two CTAs per SM so one
-// CTA's per-pixel phase overlaps the other's DMMA phases.
-template <int MODE, int PT, int RTW, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_pass(PassArgs pa) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const Dims& d = pa.d;
-  const SmemLayout lay = smem_layout(d, 1);
-  float* xs = reinterpret_cast<float*>(smem + lay.xs_off);
-  double* ws = reinterpret_cast<double*>(smem + lay.ws_off);
-  double* ss = reinterpret_cast<double*>(smem + lay.ss_off);
-  double* sh = reinterpret_cast<double*>(smem + lay.sh_off);
-  double* st = reinterpret_cast<double*>(smem + lay.st_off);
-  double* gs = reinterpret_cast<double*>(smem + lay.gs_off);
-  double* m_run = reinterpret_cast<double*>(smem + lay.col_off);
-  double* S_run = m_run + d.QCpad;
-  double* fac = S_run + d.QCpad;
-  double* hmax = fac + d.QCpad;
-  double* hsum = hmax + d.QCpad;
-  double* obj_run = hsum + d.QCpad;
-  double* hobj = obj_run + d.RC;
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int slice = blockIdx.x;
-  const int chunk = blockIdx.y;
-  const int p = d.p;
-  const int run0 = chunk * d.RC;
-  const int RCe = min(d.RC, d.M - run0);  // runs present in this chunk
-  const int ncol_valid = RCe * p;
-  const int nCT = d.QCpad / 8;
-  const int nRTx = d.Lpad / 8;
-  const int nRT = (MODE == kModeA) ? nRTx + d.QCpad / 8 : nRTx;
-  const int WST = w_stride(d.QCpad);
-  const int col0 = chunk * d.QCpad;
-  const int srow0 = run0 * p;  // first state row (A / Lg) of this chunk
-
-  const int tile_begin = static_cast<int>((static_cast<long long>(slice) * d.ntiles) / d.nslices);
-  const int tile_end = static_cast<int>((static_cast<long long>(slice + 1) * d.ntiles) / d.nslices);
-
-  // first tile in flight while the constants are staged
-  load_tile<MODE>(pa, xs, st, tile_begin * kNP, srow0, ncol_valid);
-
-  // ---- one-time staging: W chunk, G blocks, zero pad rows, running state ----
-  if (MODE == kModeA || MODE == kModeB || MODE == kModeObj) {
-    for (int e = tid; e < d.Lpad * d.QCpad; e += kThreads) {
-      const int l = e / d.QCpad, c = e % d.QCpad;
-      ws[l * WST + c] = pa.W[static_cast<size_t>(l) * d.Qs + col0 + c];
-    }
-  }
-  if (MODE == kModeA || MODE == kModeObj) {
-    for (int e = tid; e < RCe * p * p; e += kThreads) {
-      const int rl = e / (p * p), rem = e % (p * p);
-      const int i = rem / p, m = rem % p;
-      gs[e] = pa.Gbuf[static_cast<size_t>(rl * p + i) * d.Qs + col0 + rl * p + m];
-    }
-  }
-  for (int e = tid; e < (d.Lpad - d.L) * kNP; e += kThreads)
-    xs[(d.L + e / kNP) * kXST + e % kNP] = 0.0f;
-  if (tid < d.QCpad) {
-    m_run[tid] = -INFINITY;
-    S_run[tid] = 0.0;
-    fac[tid] = 1.0;
-  }
-  if (tid < d.RC) obj_run[tid] = 0.0;
-
-  double acc[RTW][kMaxCT][2];
-#pragma unroll
-  for (int i = 0; i < RTW; ++i)
-#pragma unroll
-    for (int c = 0; c < kMaxCT; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
-
-  for (int tile = tile_begin; tile < tile_end; ++tile) {
-    const int j0 = tile * kNP;
-    cp_async_wait0();
-    __syncthreads();
-
-    // ---- phase 1: S[c][j] = Σ_l W[l][c]·X[l][j]  (DMMA; warp = 8 pixels × one band half) ----
-    if (MODE != kModeInit) {
-      const int pt = warp & 3, half = warp >> 2;
-      const int kh = d.Lpad / 8;  // k-steps per band half
-      double c1[kMaxCT][2];
-#pragma unroll
-      for (int c = 0; c < kMaxCT; ++c) c1[c][0] = c1[c][1] = 0.0;
-      const float* xcol = xs + pt * 8 + g;
-      const double* wcol = ws + g;
-      for (int kk = half * kh; kk < (half + 1) * kh; ++kk) {
-        const int l = kk * 4 + t4;
-        const double bx = static_cast<double>(xcol[l * kXST]);
-#pragma unroll
-        for (int ct = 0; ct < kMaxCT; ++ct)
-          if (ct < nCT) dmma(c1[ct], wcol[l * WST + ct * 8], bx);
-      }
-      double* dst = half ? sh : ss;
-#pragma unroll
-      for (int ct = 0; ct < kMaxCT; ++ct)
-        if (ct < nCT)
-          *reinterpret_cast<double2*>(dst + (ct * 8 + g) * kSST + pt * 8 + 2 * t4) =
-              make_double2(c1[ct][0], c1[ct][1]);
-    }
-    __syncthreads();
-
-    // ---- phase 2: per-pixel updates ----
-    if (MODE == kModeA || MODE == kModeObj) {
-      constexpr int TPP = LanesPerPixel<PT>::value;
-      for (int q2 = tid; q2 < RCe * kNP * TPP; q2 += kThreads) {  // warp-uniform trip count
-        const int q = q2 / TPP, sub = q2 % TPP;
-        const int rl = q / kNP, j = q % kNP;
-        const int pix = j0 + j;
-        double o = pixel_a_update<PT, TPP, MODE == kModeA>(pa, run0 + rl, rl, j, pix, pix < d.N, sub,
-                                                             ss, sh, st, gs);
-        o = warp_sum(o);
-        if (lane == 0) hobj[q2 >> 5] = o;  // warp-task q2/32 belongs to run (q2/32)/TPP
-      }
-      if (MODE == kModeA)
-        for (int e = tid; e < (d.QCpad - ncol_valid) * kNP; e += kThreads)
-          ss[(ncol_valid + e / kNP) * kSST + e % kNP] = 0.0;
-      __syncthreads();
-      if (tid < RCe) {
-        double o = obj_run[tid];
-        for (int h = 0; h < TPP; ++h) o += hobj[tid * TPP + h];
-        obj_run[tid] = o;
-      }
-      if (MODE == kModeObj) {
-        __syncthreads();
-        if (tile + 1 < tile_end) load_tile<MODE>(pa, xs, st, j0 + kNP, srow0, ncol_valid);
-        continue;
-      }
-    } else {  // B step or B⁰ initialisation: new logits, online column max
-      constexpr int kPer = kQMax * kNP / kThreads;  // elements per thread at QCpad = kQMax
-      double ell[kPer];
-      const int per = d.QCpad * kNP / kThreads;
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        if (k < per) {
-          const int e = tid + k * kThreads;  // warp = one column × 32 pixels
-          const int c = e / kNP, j = e % kNP;
-          const int pix = j0 + j;
-          double v = -INFINITY;
-          if (c < ncol_valid && pix < d.N) {
-            const int rl = c / p, i = c % p, r = run0 + rl;
-            if (MODE == kModeInit) {
-              // solver.cpp:122-127: column i consumes draws i·N .. i·N+N−1.
-              v = 0.1 * splitmix_unit_at(pa.seeds[r], static_cast<uint64_t>(i) * d.N +
-                                                          static_cast<uint64_t>(pix));
-            } else {
-              const int gc = col0 + c;
-              double lb = st[c * kNP + j] - pa.colm[gc] - pa.collogS[gc];  // log b_old
-              lb = (lb < log_floor()) ? log_floor() : lb;                   // log max(b, 1e-30)
-              v = lb + (ss[c * kSST + j] + sh[c * kSST + j]) * pa.eta_b[r]; // + η_b·(−∇_B)
-            }
-            pa.Lg[static_cast<size_t>(srow0 + c) * d.Npad + pix] = v;
-          }
-          ell[k] = v;
-          const double hm = warp_max(v);
-          if (lane == 0) hmax[c] = hm;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        if (k < per) {
-          const int e = tid + k * kThreads;
-          const int c = e / kNP, j = e % kNP;
-          const double mn = fmax(m_run[c], hmax[c]);
-          const double w = (mn == -INFINITY) ? 0.0 : exp(ell[k] - mn);
-          ss[c * kSST + j] = w;
-          const double hs = warp_sum(w);
-          if (lane == 0) hsum[c] = hs;
-        }
-      }
-      __syncthreads();
-      if (tid < d.QCpad) {
-        const double mo = m_run[tid];
-        const double mn = fmax(mo, hmax[tid]);
-        const double f = (mn == -INFINITY || mn == mo) ? 1.0 : exp(mo - mn);
-        fac[tid] = f;
-        S_run[tid] = S_run[tid] * f + hsum[tid];
-        m_run[tid] = mn;
-      }
-      __syncthreads();
-      // rescale running accumulators to the new column max
-#pragma unroll
-      for (int ct = 0; ct < kMaxCT; ++ct) {
-        if (ct < nCT) {
-          const double f0 = fac[ct * 8 + 2 * t4], f1 = fac[ct * 8 + 2 * t4 + 1];
-          if (f0 != 1.0 || f1 != 1.0) {
-#pragma unroll
-            for (int i = 0; i < RTW; ++i) {
-              acc[i][ct][0] *= f0;
-              acc[i][ct][1] *= f1;
-            }
-          }
-        }
-      }
-    }
-
-    // ---- phase 3: C[l][c] += Σ_j X[l][j]·w[c][j]  (DMMA, warp owns row tiles) ----
-    {
-      const double* wrow = ss + g * kSST + t4;
-#pragma unroll 2
-      for (int kk = 0; kk < kNP / 4; ++kk) {
-        double bw[kMaxCT];
-#pragma unroll
-        for (int ct = 0; ct < kMaxCT; ++ct) bw[ct] = (ct < nCT) ? wrow[ct * 8 * kSST + kk * 4] : 0.0;
-#pragma unroll
-        for (int i = 0; i < RTW; ++i) {
-          const int rt = warp + 8 * i;
-          if (rt < nRT) {
-            double ax;
-            if (rt < nRTx)
-              ax = static_cast<double>(xs[(rt * 8 + g) * kXST + kk * 4 + t4]);
-            else
-              ax = ss[((rt - nRTx) * 8 + g) * kSST + kk * 4 + t4];
-#pragma unroll
-            for (int ct = 0; ct < kMaxCT; ++ct)
-              if (ct < nCT) dmma(acc[i][ct], ax, bw[ct]);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (tile + 1 < tile_end) load_tile<MODE>(pa, xs, st, j0 + kNP, srow0, ncol_valid);
-  }
-
-  // ---- write this CTA's partials ----
-  if (MODE != kModeObj) {
-#pragma unroll
-    for (int i = 0; i < RTW; ++i) {
-      const int rt = warp + 8 * i;
-      if (rt < nRT) {
-        const int row = rt * 8 + g;
-#pragma unroll
-        for (int ct = 0; ct < kMaxCT; ++ct) {
-          if (ct < nCT) {
-            double* dst = pa.part_C + (static_cast<size_t>(slice) * d.Lrows + row) * d.Qs + col0 +
-                          ct * 8 + 2 * t4;
-            *reinterpret_cast<double2*>(dst) = make_double2(acc[i][ct][0], acc[i][ct][1]);
-          }
-        }
-      }
-    }
-  }
-  if (MODE == kModeB || MODE == kModeInit) {
-    if (tid < d.QCpad) {
-      pa.part_m[static_cast<size_t>(slice) * d.Qs + col0 + tid] = m_run[tid];
-      pa.part_S[static_cast<size_t>(slice) * d.Qs + col0 + tid] = S_run[tid];
-    }
-  } else {
-    if (tid < RCe) pa.part_obj[static_cast<size_t>(slice) * d.M + run0 + tid] = obj_run[tid];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Combine, B/init: per column the log-sum-exp merge of the slice partials,
-// m = max_s m_s, S = Σ_s S_s·e^{m_s − m}; one warp per column, lanes stride
 // the slices, fixed xor-tree merge (deterministic).
 __global__ void k_colnorm(CombineArgs ca) {
   const Dims& d = ca.d;
@@ -650,7 +186,8 @@ __global__ void __launch_bounds__(256) k_post(PostArgs pa) {
   pa.eta_b[r] = __dmul_rn(sqrt(static_cast<double>(p) / static_cast<double>(d.N)), ea);
 }
 
-__global__ void k_xnorm(const float* X, double* xnorm, Dims d) {
+template <class XT>
+__global__ void k_xnorm(const XT* X, double* xnorm, Dims d) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d.Npad) return;
   double s = 0.0;
@@ -677,8 +214,9 @@ __global__ void k_materialize_b(const double* Lg, const double* colm, const doub
 // E = X·B̂ in the reference's accumulation order (matrix.cpp:64-73: pixel
 // index ascending, multiply then add, from 0.0) so E is bitwise the host
 // matmul(X, B̂) of the same fp32-exact X. Output [M][Lpad][p].
-__global__ void __launch_bounds__(256) k_strict_e(const float* X, const double* Bv, double* E, Dims d) {
-  __shared__ float xs[32][65];
+template <class XT>
+__global__ void __launch_bounds__(256) k_strict_e(const XT* X, const double* Bv, double* E, Dims d) {
+  __shared__ double xs[32][65];
   __shared__ double bs[32][65];
   const int lane = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const int l0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
@@ -688,7 +226,7 @@ __global__ void __launch_bounds__(256) k_strict_e(const float* X, const double* 
     for (int e = threadIdx.x; e < 32 * 64; e += 256) {
       const int rr = e / 64, jj = e % 64;
       const int l = l0 + rr, c = c0 + rr, j = j0 + jj;
-      xs[rr][jj] = (l < d.L && j < d.N) ? X[static_cast<size_t>(l) * d.Npad + j] : 0.0f;
+      xs[rr][jj] = (l < d.L && j < d.N) ? static_cast<double>(X[static_cast<size_t>(l) * d.Npad + j]) : 0.0;
       bs[rr][jj] = (c < ncol && j < d.N) ? Bv[static_cast<size_t>(c) * d.Npad + j] : 0.0;
     }
     __syncthreads();
@@ -715,7 +253,8 @@ __global__ void __launch_bounds__(256) k_strict_e(const float* X, const double* 
 // follows matmul's order (endmember index ascending, multiply then add);
 // the sum over elements is a fixed-order tree (per block) then a fixed-order
 // sum over blocks.
-__global__ void __launch_bounds__(256) k_fit_partial(const float* X, const double* E, const double* A,
+template <class XT>
+__global__ void __launch_bounds__(256) k_fit_partial(const XT* X, const double* E, const double* A,
                                                      double* part, int nblk, Dims d) {
   __shared__ double es[kMaxLpad * kMaxP];
   __shared__ double red[256];
@@ -795,60 +334,17 @@ __global__ void k_select(const double* fit, const double* mu, const int* fail_co
   *fit_min = fmin;
 }
 
-template <int MODE, int RTW>
-cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
-  constexpr int MB = (RTW <= 4) ? 2 : 1;
-  const dim3 grid(a.d.nslices, a.d.NCH);
-  const size_t smem = smem_layout(a.d, a.d.nbuf).total;
-  void (*kern)(PassArgs) = nullptr;
-  if (MODE == kModeInit || MODE == kModeB) {
-    kern = k_pass<MODE, 1, RTW, MB>;
-  } else {
-    switch (pt) {
-#define EDAA_PT_CASE(P)                                       \
-  case P:                                                     \
-    kern = k_pass<MODE, P, RTW, (P <= 12 ? MB : 1)>;          \
-    break;
-      EDAA_PT_CASE(2) EDAA_PT_CASE(3) EDAA_PT_CASE(4) EDAA_PT_CASE(5) EDAA_PT_CASE(6)
-      EDAA_PT_CASE(7) EDAA_PT_CASE(8) EDAA_PT_CASE(10) EDAA_PT_CASE(12) EDAA_PT_CASE(16)
-#undef EDAA_PT_CASE
-      default:
-        return cudaErrorInvalidValue;
-    }
-  }
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-int pt_bucket(int p) {
-  if (p <= 8) return p;
-  if (p <= 10) return 10;
-  if (p <= 12) return 12;
-  return 16;
-}
-
 }  // namespace
 
-size_t pass_smem_bytes(const Dims& d, int nbuf) { return smem_layout(d, nbuf).total; }
+size_t pass_smem_bytes(const Dims& d, int nbuf) { return dev::smem_layout(d, nbuf).total; }
+
+cudaError_t launch_pass_f32(int mode, const PassArgs& a, cudaStream_t st);
+cudaError_t launch_pass_f64(int mode, const PassArgs& a, cudaStream_t st);
 
 cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st) {
-  const int pt = pt_bucket(a.d.p);
-  const bool wide = (a.d.Lpad / 8 + a.d.QCpad / 8) > 32;  // > 4 row tiles per warp
-  switch (mode) {
-    case kModeInit:
-      return wide ? launch_pass_rtw<kModeInit, 6>(a, st, pt) : launch_pass_rtw<kModeInit, 4>(a, st, pt);
-    case kModeA:
-      return wide ? launch_pass_rtw<kModeA, 6>(a, st, pt) : launch_pass_rtw<kModeA, 4>(a, st, pt);
-    case kModeB:
-      return wide ? launch_pass_rtw<kModeB, 6>(a, st, pt) : launch_pass_rtw<kModeB, 4>(a, st, pt);
-    case kModeObj:
-      return launch_pass_rtw<kModeObj, 1>(a, st, pt);
-  }
-  return cudaErrorInvalidValue;
+  return a.d.xbytes == 8 ? launch_pass_f64(mode, a, st) : launch_pass_f32(mode, a, st);
 }
+
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   const Dims& d = a.d;
@@ -868,8 +364,11 @@ cudaError_t launch_post(const PostArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_xnorm(const float* X, double* xnorm, const Dims& d, cudaStream_t st) {
-  k_xnorm<<<(d.Npad + 255) / 256, 256, 0, st>>>(X, xnorm, d);
+cudaError_t launch_xnorm(const void* X, double* xnorm, const Dims& d, cudaStream_t st) {
+  if (d.xbytes == 8)
+    k_xnorm<<<(d.Npad + 255) / 256, 256, 0, st>>>(static_cast<const double*>(X), xnorm, d);
+  else
+    k_xnorm<<<(d.Npad + 255) / 256, 256, 0, st>>>(static_cast<const float*>(X), xnorm, d);
   return cudaGetLastError();
 }
 
@@ -880,16 +379,22 @@ cudaError_t launch_materialize_b(const double* Lg, const double* colm, const dou
   return cudaGetLastError();
 }
 
-cudaError_t launch_strict_e(const float* X, const double* Bv, double* E, const Dims& d,
+cudaError_t launch_strict_e(const void* X, const double* Bv, double* E, const Dims& d,
                             cudaStream_t st) {
   const dim3 grid((d.L + 31) / 32, (d.M * d.p + 31) / 32);
-  k_strict_e<<<grid, 256, 0, st>>>(X, Bv, E, d);
+  if (d.xbytes == 8)
+    k_strict_e<<<grid, 256, 0, st>>>(static_cast<const double*>(X), Bv, E, d);
+  else
+    k_strict_e<<<grid, 256, 0, st>>>(static_cast<const float*>(X), Bv, E, d);
   return cudaGetLastError();
 }
 
-cudaError_t launch_fit(const float* X, const double* E, const double* A, double* part_fit,
+cudaError_t launch_fit(const void* X, const double* E, const double* A, double* part_fit,
                        double* fit, int fit_blocks, const Dims& d, cudaStream_t st) {
-  k_fit_partial<<<dim3(fit_blocks, d.M), 256, 0, st>>>(X, E, A, part_fit, fit_blocks, d);
+  if (d.xbytes == 8)
+    k_fit_partial<<<dim3(fit_blocks, d.M), 256, 0, st>>>(static_cast<const double*>(X), E, A, part_fit, fit_blocks, d);
+  else
+    k_fit_partial<<<dim3(fit_blocks, d.M), 256, 0, st>>>(static_cast<const float*>(X), E, A, part_fit, fit_blocks, d);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_fit_final<<<(d.M + 127) / 128, 128, 0, st>>>(part_fit, fit, fit_blocks, d.M);

@@ -153,7 +153,11 @@ def select_runs(per_run: List[RunRecord], fit_slack: float) -> SelectionReport:
 
 
 def validate_image(x) -> np.ndarray:
-    """HsiImage::validate (image.cpp:10-27) on the L×N data; returns fp32 X."""
+    """HsiImage::validate (image.cpp:10-27) on the L×N data.
+
+    Returns the array the device will hold: fp32 when every value is exactly an
+    fp32 (the fast path, two CTAs per SM), otherwise fp64 so that results track
+    the reference on any fp64 input."""
     arr = np.asarray(x)
     if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
         raise EdaaError("image: needs at least one band and one pixel")
@@ -161,7 +165,13 @@ def validate_image(x) -> np.ndarray:
         raise EdaaError("image: non-finite reflectance")
     if np.any(arr < 0):
         raise EdaaError("image: negative reflectance")
-    return np.ascontiguousarray(arr, dtype=np.float32)
+    if arr.dtype == np.float32:
+        return np.ascontiguousarray(arr)
+    a64 = np.ascontiguousarray(arr, dtype=np.float64)
+    a32 = a64.astype(np.float32)
+    if np.array_equal(a32.astype(np.float64), a64):
+        return a32
+    return a64
 
 
 class Device:
@@ -216,10 +226,12 @@ class Device:
                                                        x.shape[0], x.shape[1], x.stride(0)))
             self.L, self.N = int(x.shape[0]), int(x.shape[1])
             return
-        xf = np.ascontiguousarray(x, dtype=np.float32)
+        xf = np.ascontiguousarray(x)
+        if xf.dtype != np.float64:
+            xf = np.ascontiguousarray(xf, dtype=np.float32)
         self._x_keep = xf
-        self._check(self.lib.edaa_set_image_host(self.h, xf.ctypes.data_as(C.c_void_p),
-                                                 xf.shape[0], xf.shape[1]))
+        fn = self.lib.edaa_set_image_host_f64 if xf.dtype == np.float64 else self.lib.edaa_set_image_host
+        self._check(fn(self.h, xf.ctypes.data_as(C.c_void_p), xf.shape[0], xf.shape[1]))
         self.L, self.N = xf.shape
 
     # -- solve ------------------------------------------------------------------
