@@ -124,6 +124,26 @@ typedef void (*edaa_observer_fn)(size_t outer, char block, size_t inner, const d
 EDAA_API int edaa_solve_observed(edaa_ctx* ctx, const edaa_solve_params* params, edaa_observer_fn fn,
                         void* user);
 
+/* Single-evaluation primitives on the image of the context (reference
+ * solver.hpp:52-67,85-86 and ensemble.hpp:50).  Host arrays in the
+ * reference layouts (b: N×p, a: p×N, e: L×p); entries follow the reference's
+ * accumulation order.
+ *   edaa_xb                   y = X·B (L×p)               — matmul(x, b), solver.cpp:140
+ *   edaa_objective            ½‖X − XB·A‖²               — objective_l2, solver.cpp:184-188
+ *   edaa_grad_abundances      g = −(XB)ᵀ(X − XBA)  (p×N)  — solver.cpp:166-172
+ *   edaa_grad_contributions   g = −Xᵀ((X − XBA)Aᵀ) (N×p)  — solver.cpp:174-182
+ *   edaa_fit_l1               Σ|X − E·A|                  — ensemble.cpp:29-39
+ *   edaa_estimate_abundances  A for fixed E, `iters` entropic steps from 1/p
+ *                                                          — solver.cpp:240-259 */
+EDAA_API int edaa_xb(edaa_ctx* ctx, const double* b, size_t p, double* y);
+EDAA_API int edaa_objective(edaa_ctx* ctx, const double* b, const double* a, size_t p, double* out);
+EDAA_API int edaa_grad_abundances(edaa_ctx* ctx, const double* b, const double* a, size_t p, double* g);
+EDAA_API int edaa_grad_contributions(edaa_ctx* ctx, const double* b, const double* a, size_t p,
+                                     double* g);
+EDAA_API int edaa_fit_l1(edaa_ctx* ctx, const double* e, const double* a, size_t p, double* out);
+EDAA_API int edaa_estimate_abundances(edaa_ctx* ctx, const double* e, size_t p, size_t iters,
+                                      double eta, double* a);
+
 /* Instrumentation.  With profiling on, every pass launch is bracketed by CUDA
  * events on edaa_stream(); edaa_profile_read returns, per pass kind, the
  * summed device time (ms) and launch count of the last finished solve

@@ -63,6 +63,14 @@ SIGNATURES = [
                               C.POINTER(C.c_double)]),
     ("edaa_solve_observed", C.c_int, [C.c_void_p, C.POINTER(SolveParams), OBSERVER_FN,
                                       C.c_void_p]),
+    ("edaa_xb", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("edaa_objective", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("edaa_grad_abundances", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("edaa_grad_contributions", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                          C.c_void_p]),
+    ("edaa_fit_l1", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("edaa_estimate_abundances", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
+                                           C.c_double, C.c_void_p]),
     ("edaa_profile_enable", C.c_int, [C.c_void_p, C.c_int]),
     ("edaa_profile_read", C.c_int, [C.c_void_p, C.POINTER(ProfileC)]),
     ("edaa_launch_count", C.c_uint64, [C.c_void_p]),

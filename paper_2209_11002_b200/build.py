@@ -24,7 +24,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                   "-I" + os.path.join(ROOT, "include")]
-CUDA_SRCS = ["edaa_pass_f32.cu", "edaa_pass_f64.cu", "edaa_kernels.cu", "edaa_capi.cu"]
+CUDA_SRCS = ["edaa_pass_f32.cu", "edaa_pass_f64.cu", "edaa_kernels.cu", "edaa_prims.cu",
+             "edaa_capi.cu"]
 HOST_SRCS = ["matrix.cpp", "image.cpp", "types.cpp", "solver.cpp", "ensemble.cpp", "device.cpp"]
 
 CUDA_LIB = os.path.join(PKG, "libedaa_cuda.so")
@@ -61,7 +62,7 @@ def build_cuda(force=False, verbose=False):
             if verbose and out:
                 print(out)
     if force or _stale(CUDA_LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", CUDA_LIB] + objs + ["-lcudart"])
+        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", CUDA_LIB] + objs)
     return CUDA_LIB
 
 

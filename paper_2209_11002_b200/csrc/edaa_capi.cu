@@ -41,7 +41,7 @@ struct edaa_ctx {
   };
   Buf A, Lg, Bv, Y, Z, XAt, AAt, Gbuf, colm, colS, collogS, eta_a, eta_b, gamma, trace, part_C,
       part_m, part_S, part_obj, fac, E, fit, mu, part_fit, seeds, fail_key, fail_code, fail_value, cand,
-      selected, fit_min, obsA;
+      selected, fit_min, obsA, pr_b, pr_a, pr_y, pr_r, pr_g, pr_rat, pr_part, pr_out;
   int fit_blocks = 0;
   // instrumentation
   bool profile = false;
@@ -482,7 +482,9 @@ int edaa_destroy(edaa_ctx* c) {
                            &c->colm, &c->colS, &c->collogS, &c->eta_a, &c->eta_b, &c->gamma,
                            &c->trace, &c->part_C, &c->part_m, &c->part_S, &c->part_obj, &c->fac, &c->E,
                            &c->fit, &c->mu, &c->part_fit, &c->seeds, &c->fail_key, &c->fail_code,
-                           &c->fail_value, &c->cand, &c->selected, &c->fit_min, &c->obsA};
+                           &c->fail_value, &c->cand, &c->selected, &c->fit_min, &c->obsA,
+                           &c->pr_b, &c->pr_a, &c->pr_y, &c->pr_r, &c->pr_g, &c->pr_rat,
+                           &c->pr_part, &c->pr_out};
   for (auto* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->X) cudaFree(c->X);
@@ -743,6 +745,150 @@ int edaa_solve_observed(edaa_ctx* c, const edaa_solve_params* prm, edaa_observer
   int rc = solve_impl(c, prm, &hook);
   if (rc) return rc;
   return edaa_finish(c);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Single-evaluation primitives on the image set in the context.
+namespace {
+
+Dims prim_dims(edaa_ctx* c, size_t p) {
+  Dims d{};
+  d.L = c->L;
+  d.Lpad = (c->L + 7) / 8 * 8;
+  d.N = c->N;
+  d.Npad = c->Npad;
+  d.M = 1;
+  d.p = static_cast<int>(p);
+  d.xbytes = c->xbytes;
+  return d;
+}
+
+// Upload a host p×N (row-major) matrix as [p][Npad] with zero padding.
+int upload_pn(edaa_ctx* c, edaa_ctx::Buf& buf, const double* a, size_t p) {
+  const size_t pitch = static_cast<size_t>(c->Npad) * 8;
+  EDAA_CUDA(c, ensure(buf, p * pitch));
+  EDAA_CUDA(c, cudaMemsetAsync(buf.p, 0, p * pitch, c->stream));
+  EDAA_CUDA(c, cudaMemcpy2DAsync(buf.p, pitch, a, c->N * 8, c->N * 8, p, cudaMemcpyHostToDevice, c->stream));
+  return EDAA_OK;
+}
+
+// Y = X·B (L×p, reference order) from a host N×p B; Y stays in c->pr_y as [L][p].
+int device_xb(edaa_ctx* c, const double* b, size_t p) {
+  std::vector<double> bt(p * c->N);
+  for (int j = 0; j < c->N; ++j)
+    for (size_t i = 0; i < p; ++i) bt[i * c->N + j] = b[static_cast<size_t>(j) * p + i];
+  int rc = upload_pn(c, c->pr_b, bt.data(), p);
+  if (rc) return rc;
+  const Dims d = prim_dims(c, p);
+  EDAA_CUDA(c, ensure(c->pr_y, static_cast<size_t>(d.Lpad) * p * 8));
+  EDAA_LAUNCH(c, edaa::launch_strict_e(c->X, P<double>(c->pr_b), P<double>(c->pr_y), d, c->stream));
+  return EDAA_OK;
+}
+
+int residual_from(edaa_ctx* c, const double* a, size_t p) {
+  int rc = upload_pn(c, c->pr_a, a, p);
+  if (rc) return rc;
+  EDAA_CUDA(c, ensure(c->pr_r, static_cast<size_t>(c->L) * c->Npad * 8));
+  EDAA_LAUNCH(c, edaa::launch_residual(c->X, c->xbytes, P<double>(c->pr_y), P<double>(c->pr_a),
+                                       P<double>(c->pr_r), c->L, c->N, c->Npad, static_cast<int>(p), c->stream));
+  return EDAA_OK;
+}
+
+int reduce_r(edaa_ctx* c, int mode, double scale, double* out) {
+  const int parts = 256;
+  EDAA_CUDA(c, ensure(c->pr_part, parts * 8));
+  EDAA_CUDA(c, ensure(c->pr_out, 8));
+  EDAA_LAUNCH_N(c, edaa::launch_reduce(P<double>(c->pr_r), static_cast<size_t>(c->L) * c->Npad, mode,
+                                       scale, P<double>(c->pr_part), parts, P<double>(c->pr_out), c->stream), 2);
+  EDAA_CUDA(c, cudaMemcpyAsync(out, c->pr_out.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  return EDAA_OK;
+}
+
+int prim_check(edaa_ctx* c, size_t p, const void* a, const void* b) {
+  if (!c || !a || !b) return set_err(c, EDAA_ERR_INVALID, "null argument");
+  if (c->X == nullptr) return set_err(c, EDAA_ERR_STATE, "no image set");
+  if (p < 1) return set_err(c, EDAA_ERR_INVALID, "need at least one endmember");
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  return EDAA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int edaa_xb(edaa_ctx* c, const double* b, size_t p, double* y) {
+  int rc = prim_check(c, p, b, y);
+  if (rc) return rc;
+  rc = device_xb(c, b, p);
+  if (rc) return rc;
+  EDAA_CUDA(c, cudaMemcpyAsync(y, c->pr_y.p, static_cast<size_t>(c->L) * p * 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  return EDAA_OK;
+}
+
+int edaa_objective(edaa_ctx* c, const double* b, const double* a, size_t p, double* out) {
+  int rc = prim_check(c, p, b, a);
+  if (!rc) rc = device_xb(c, b, p);
+  if (!rc) rc = residual_from(c, a, p);
+  if (!rc) rc = reduce_r(c, 0, 0.5, out);
+  return rc;
+}
+
+int edaa_fit_l1(edaa_ctx* c, const double* e, const double* a, size_t p, double* out) {
+  int rc = prim_check(c, p, e, a);
+  if (rc) return rc;
+  EDAA_CUDA(c, ensure(c->pr_y, static_cast<size_t>(c->L) * p * 8));
+  EDAA_CUDA(c, cudaMemcpyAsync(c->pr_y.p, e, static_cast<size_t>(c->L) * p * 8, cudaMemcpyHostToDevice, c->stream));
+  rc = residual_from(c, a, p);
+  if (!rc) rc = reduce_r(c, 1, 1.0, out);
+  return rc;
+}
+
+int edaa_grad_abundances(edaa_ctx* c, const double* b, const double* a, size_t p, double* g) {
+  int rc = prim_check(c, p, b, a);
+  if (!rc) rc = device_xb(c, b, p);
+  if (!rc) rc = residual_from(c, a, p);
+  if (rc) return rc;
+  EDAA_CUDA(c, ensure(c->pr_g, p * c->N * 8));
+  EDAA_LAUNCH(c, edaa::launch_grad_a(P<double>(c->pr_y), P<double>(c->pr_r), P<double>(c->pr_g), c->L,
+                                     c->N, c->Npad, static_cast<int>(p), c->stream));
+  EDAA_CUDA(c, cudaMemcpyAsync(g, c->pr_g.p, p * c->N * 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  return EDAA_OK;
+}
+
+int edaa_grad_contributions(edaa_ctx* c, const double* b, const double* a, size_t p, double* g) {
+  int rc = prim_check(c, p, b, a);
+  if (!rc) rc = device_xb(c, b, p);
+  if (!rc) rc = residual_from(c, a, p);
+  if (rc) return rc;
+  EDAA_CUDA(c, ensure(c->pr_g, p * c->N * 8));
+  EDAA_CUDA(c, ensure(c->pr_rat, static_cast<size_t>(c->L) * p * 8));
+  EDAA_LAUNCH_N(c, edaa::launch_grad_b(c->X, c->xbytes, P<double>(c->pr_r), P<double>(c->pr_a),
+                                       P<double>(c->pr_rat), P<double>(c->pr_g), c->L, c->N, c->Npad,
+                                       static_cast<int>(p), c->stream), 2);
+  EDAA_CUDA(c, cudaMemcpyAsync(g, c->pr_g.p, p * c->N * 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  return EDAA_OK;
+}
+
+int edaa_estimate_abundances(edaa_ctx* c, const double* e, size_t p, size_t iters, double eta,
+                             double* a) {
+  int rc = prim_check(c, p, e, a);
+  if (rc) return rc;
+  if (p > static_cast<size_t>(edaa::kMaxP))
+    return set_err(c, EDAA_ERR_UNSUPPORTED, "endmember count above the compiled maximum (16)");
+  EDAA_CUDA(c, ensure(c->pr_y, static_cast<size_t>(c->L) * p * 8));
+  EDAA_CUDA(c, cudaMemcpyAsync(c->pr_y.p, e, static_cast<size_t>(c->L) * p * 8, cudaMemcpyHostToDevice, c->stream));
+  EDAA_CUDA(c, ensure(c->pr_g, p * c->N * 8));
+  EDAA_LAUNCH(c, edaa::launch_estimate(c->X, c->xbytes, P<double>(c->pr_y), P<double>(c->pr_g), c->L, c->N,
+                                       c->Npad, static_cast<int>(p), static_cast<int>(iters), eta, c->stream));
+  EDAA_CUDA(c, cudaMemcpyAsync(a, c->pr_g.p, p * c->N * 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  return EDAA_OK;
 }
 
 }  // extern "C"

@@ -132,6 +132,17 @@ cudaError_t launch_select(const double* fit, const double* mu, const int* fail_c
                           unsigned char* cand, long long* selected, double* fit_min,
                           cudaStream_t st);
 size_t pass_smem_bytes(const Dims& d, int nbuf);
+// primitives (edaa_prims.cu)
+cudaError_t launch_residual(const void* X, int xbytes, const double* Y, const double* A, double* R,
+                            int L, int N, int Npad, int p, cudaStream_t st);
+cudaError_t launch_reduce(const double* R, size_t total, int mode, double scale, double* part,
+                          int nparts, double* out, cudaStream_t st);
+cudaError_t launch_grad_a(const double* Y, const double* R, double* G, int L, int N, int Npad, int p,
+                          cudaStream_t st);
+cudaError_t launch_grad_b(const void* X, int xbytes, const double* R, const double* A, double* rat,
+                          double* G, int L, int N, int Npad, int p, cudaStream_t st);
+cudaError_t launch_estimate(const void* X, int xbytes, const double* E, double* A, int L, int N,
+                            int Npad, int p, int iters, double eta, cudaStream_t st);
 constexpr int kMaxSmem = 232448;  // sm_100 opt-in dynamic shared memory per block
 
 }  // namespace edaa
