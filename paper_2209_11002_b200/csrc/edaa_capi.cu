@@ -173,12 +173,12 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.M = static_cast<int>(prm->runs);
   d.p = static_cast<int>(p);
   d.RC = std::max(1, std::min(edaa::kQMax / d.p, d.M));
-  d.QCpad = (d.RC * d.p + 7) / 8 * 8;
+  d.QCpad = edaa::kQMax;  // fixed 3 DMMA column tiles: unpredicated tensor-core code
   d.NCH = (d.M + d.RC - 1) / d.RC;
   d.Qs = d.NCH * d.QCpad;
   d.Lrows = d.Lpad + d.QCpad;
   d.K1 = static_cast<int>(prm->inner_iters_a);
-  d.nbuf = 1;
+  d.nbuf = (edaa::pass_smem_bytes(d, 3) <= static_cast<size_t>(edaa::kMaxSmem)) ? 3 : 2;
   if (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem))
     return set_err(c, EDAA_ERR_UNSUPPORTED, "tile working set exceeds shared memory");
   *out = d;

@@ -40,8 +40,15 @@ __device__ __forceinline__ double max_like_std(double top, double s) {
   return (top < s) ? s : top;  // std::max(top, s): NaN in s is ignored
 }
 
+// Shared-memory plan of the pass kernel (one CTA per SM, two warp groups):
+//   xs  nbuf × X tile          [Lpad][kXST] fp32/fp64  (tile i+2 loads while i, i+1 are used)
+//   ws  W chunk (Y or Z)       [Lpad][WST]  fp64
+//   ss  2 × projection/weights [QCpad][kSST] fp64 (band half 0; becomes the weights w)
+//   sh  2 × projection half 1  [QCpad][kSST] fp64
+//   st  2 × state tile         [QCpad][kNP] fp64 (A or logits of the chunk's columns)
+//   gs  G blocks of the chunk's runs, then per-column and per-run scalars.
 struct SmemLayout {
-  int xs_off, ws_off, ss_off, sh_off, st_off, gs_off, col_off, total;
+  int xs_off, xs_bytes, ws_off, ss_off, sh_off, st_off, buf_bytes, st_bytes, gs_off, col_off, total;
 };
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
@@ -49,27 +56,38 @@ __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 // W row stride (doubles): ≡ 8 mod 16 so a DMMA A-fragment (4 rows × 8 columns) hits 2 wavefronts.
 __host__ __device__ inline int w_stride(int qcpad) { return qcpad + ((qcpad % 16 == 0) ? 8 : 0); }
 
-__host__ __device__ inline SmemLayout smem_layout(const Dims& d, int /*nbuf*/) {
-  const int xb = d.xbytes;
+__host__ __device__ inline SmemLayout smem_layout(const Dims& d, int nbuf) {
   SmemLayout s;
   int off = 0;
-  s.xs_off = off;  // X tile, fp32 or fp64 [Lpad][kXST]
-  off += align16(d.Lpad * kXST * xb);
-  s.ws_off = off;  // W chunk, fp64 [Lpad][WST]
+  s.xs_off = off;
+  s.xs_bytes = align16(d.Lpad * kXST * d.xbytes);
+  off += nbuf * s.xs_bytes;
+  s.ws_off = off;
   off += align16(d.Lpad * w_stride(d.QCpad) * 8);
-  s.ss_off = off;  // projection / weights, fp64 [QCpad][kSST]
-  off += align16(d.QCpad * kSST * 8);
-  s.sh_off = off;  // second half of the band-split projection
-  off += align16(d.QCpad * kSST * 8);
-  s.st_off = off;  // state tile (A or logits) of the chunk, fp64 [QCpad][kNP]
-  off += align16(d.QCpad * kNP * 8);
+  s.buf_bytes = align16(d.QCpad * kSST * 8);
+  s.ss_off = off;
+  off += 2 * s.buf_bytes;
+  s.sh_off = off;
+  off += 2 * s.buf_bytes;
+  s.st_bytes = align16(d.QCpad * kNP * 8);
+  s.st_off = off;
+  off += 2 * s.st_bytes;
   s.gs_off = off;
   off += align16(d.RC * d.p * d.p * 8);
-  s.col_off = off;  // m_run, S_run, fac, hmax, hsum (QCpad each) + obj_run (RC), hobj (4·RC)
-  off += align16((5 * d.QCpad + 5 * d.RC) * 8);
+  // m_run, S_run, colm, collogS, eta (QCpad each), fac[2][QCpad]; obj_run (RC), hobj (4·RC)
+  s.col_off = off;
+  off += align16((7 * d.QCpad + 5 * d.RC) * 8);
   s.total = off;
   return s;
 }
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll

@@ -21,7 +21,8 @@
 
 namespace edaa {
 
-constexpr int kThreads = 256;   // 8 warps per CTA, two CTAs per SM
+constexpr int kThreads = 512;   // 16 warps per CTA: 8 MMA warps + 8 update warps
+constexpr int kGroup = 256;     // threads per warp group
 constexpr int kNP = 32;         // pixels per tile
 constexpr int kXST = kNP + 8;   // fp32 X tile row stride (conflict-free DMMA B-frags)
 constexpr int kSST = kNP + 4;   // fp64 weight tile row stride
