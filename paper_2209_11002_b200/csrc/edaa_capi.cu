@@ -10,14 +10,17 @@
 //   objective pass (trace[T]) → combine; materialise B; E = X·B (reference
 //   order); fit_l1; coherence.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "../../include/edaa_b200.h"
-#include "edaa_internal.cuh"
+#include "edaa_device.cuh"
 
 using edaa::Dims;
 
@@ -50,6 +53,10 @@ struct edaa_ctx {
   size_t ev_used = 0;
   edaa_profile last_prof{};
   uint64_t launches = 0;
+  void* kprof_buf = nullptr;  // EDAA_KPROF=1: per-phase cycle counters (dev only)
+  int dbg = 0;                // EDAA_DBG: development switches, results invalid when set
+  int num_sms = 148;
+  alignas(64) CUtensorMap xmap;  // TMA descriptor of X for the current solve
   // host copies of the per-run records
   std::vector<double> h_fit, h_mu, h_eta_a, h_eta_b, h_fail_value, h_trace;
   std::vector<int> h_fail_code;
@@ -178,10 +185,39 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.Qs = d.NCH * d.QCpad;
   d.Lrows = d.Lpad + d.QCpad;
   d.K1 = static_cast<int>(prm->inner_iters_a);
+  d.ncta = c->num_sms;
   d.nbuf = (edaa::pass_smem_bytes(d, 3) <= static_cast<size_t>(edaa::kMaxSmem)) ? 3 : 2;
   if (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem))
     return set_err(c, EDAA_ERR_UNSUPPORTED, "tile working set exceeds shared memory");
   *out = d;
+  return EDAA_OK;
+}
+
+// TMA descriptor of X: 2-D [L][Npad] (inner dimension = pixels), boxes of 128 bytes
+// × x_box_rows rows with 128-byte swizzle; rows ≥ L read as zeros.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_xmap(edaa_ctx* c, const Dims& d) {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return set_err(c, EDAA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const int esz = d.xbytes;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.Npad), static_cast<cuuint64_t>(d.L)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.Npad) * esz};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(edaa::dev::x_box_rows(d))};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&c->xmap, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                            c->X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(c, EDAA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return EDAA_OK;
 }
 
@@ -246,6 +282,9 @@ edaa::PassArgs pass_args(edaa_ctx* c, int t, const double* W) {
   a.part_obj = P<double>(c->part_obj);
   a.fail_key = P<unsigned long long>(c->fail_key);
   a.observe_A = nullptr;
+  a.kprof = static_cast<unsigned long long*>(c->kprof_buf);
+  a.dbg = c->dbg;
+  a.xmap = &c->xmap;
   return a;
 }
 
@@ -352,6 +391,8 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   c->T = prm->outer_iters;
   c->solved = false;
   rc = alloc_solve(c, d, c->T);
+  if (rc) return rc;
+  rc = make_xmap(c, d);
   if (rc) return rc;
   cudaStream_t st = c->stream;
   EDAA_CUDA(c, cudaMemcpyAsync(c->seeds.p, prm->seeds, d.M * 8, cudaMemcpyHostToDevice, st));
@@ -470,6 +511,10 @@ int edaa_create(int device, edaa_ctx** out) {
     delete c;
     return EDAA_ERR_CUDA;
   }
+  if (const char* dbg = std::getenv("EDAA_DBG")) c->dbg = std::atoi(dbg);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char* kp = std::getenv("EDAA_KPROF"))
+    if (kp[0] == '1' && cudaMalloc(&c->kprof_buf, 24 * 8) == cudaSuccess) cudaMemset(c->kprof_buf, 0, 24 * 8);
   *out = c;
   return EDAA_OK;
 }
@@ -606,6 +651,17 @@ int edaa_finish(edaa_ctx* c) {
   }
   c->ev_used = 0;
   c->solved = true;
+  if (c->kprof_buf) {
+    unsigned long long v[24];
+    cudaMemcpy(v, c->kprof_buf, sizeof v, cudaMemcpyDeviceToHost);
+    const char* names[4] = {"init", "A", "B", "obj"};
+    for (int m = 0; m < 4; ++m) {
+      const unsigned long long* w = v + 6 * m;
+      std::fprintf(stderr, "[edaa kprof] %4s mma: x_wait %llu p1 %llu w_wait %llu p3 %llu | upd: s_wait %llu p2 %llu\n",
+                   names[m], w[0], w[1], w[2], w[3], w[4], w[5]);
+    }
+    cudaMemset(c->kprof_buf, 0, sizeof v);
+  }
   return EDAA_OK;
 }
 

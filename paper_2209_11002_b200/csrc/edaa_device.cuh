@@ -48,7 +48,8 @@ __device__ __forceinline__ double max_like_std(double top, double s) {
 //   st  2 × state tile         [QCpad][kNP] fp64 (A or logits of the chunk's columns)
 //   gs  G blocks of the chunk's runs, then per-column and per-run scalars.
 struct SmemLayout {
-  int xs_off, xs_bytes, ws_off, ss_off, sh_off, st_off, buf_bytes, st_bytes, gs_off, col_off, total;
+  int xs_off, xs_bytes, ws_off, ss_off, sh_off, st_off, buf_bytes, st_bytes, gs_off, col_off, tab_off,
+      mbar_off, total;
 };
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
@@ -56,11 +57,38 @@ __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 // W row stride (doubles): ≡ 8 mod 16 so a DMMA A-fragment (4 rows × 8 columns) hits 2 wavefronts.
 __host__ __device__ inline int w_stride(int qcpad) { return qcpad + ((qcpad % 16 == 0) ? 8 : 0); }
 
+// X tiles arrive by TMA with 128-byte swizzle: each smem row holds 128 bytes
+// (32 floats, or 16 doubles — an fp64 tile is two 16-column halves).  Boxes
+// are at most 256 rows, so L > 256 takes two row boxes of x_box_rows each.
+__host__ __device__ inline int x_box_rows(const Dims& d) {
+  return d.Lpad <= 256 ? d.Lpad : ((d.Lpad / 2 + 7) / 8) * 8;
+}
+__host__ __device__ inline int x_rows(const Dims& d) {
+  const int br = x_box_rows(d);
+  return ((d.Lpad + br - 1) / br) * br;
+}
+__host__ __device__ inline int x_tile_bytes(const Dims& d) {
+  const int b = x_rows(d) * 128 * (d.xbytes / 4);
+  return (b + 1023) & ~1023;
+}
+// Element offset of X[l][j] (0 ≤ j < 32) inside a swizzled tile buffer.
+template <class XT>
+__device__ __forceinline__ int xoff(int l, int j, int rows);
+template <>
+__device__ __forceinline__ int xoff<float>(int l, int j, int /*rows*/) {
+  return l * 32 + ((((j >> 2) ^ (l & 7))) << 2) + (j & 3);
+}
+template <>
+__device__ __forceinline__ int xoff<double>(int l, int j, int rows) {
+  const int jj = j & 15;
+  return (j >> 4) * rows * 16 + l * 16 + (((jj >> 1) ^ (l & 7)) << 1) + (jj & 1);
+}
+
 __host__ __device__ inline SmemLayout smem_layout(const Dims& d, int nbuf) {
   SmemLayout s;
   int off = 0;
-  s.xs_off = off;
-  s.xs_bytes = align16(d.Lpad * kXST * d.xbytes);
+  s.xs_off = off;  // TMA destination: 1024-byte aligned, 128-byte swizzled rows
+  s.xs_bytes = x_tile_bytes(d);
   off += nbuf * s.xs_bytes;
   s.ws_off = off;
   off += align16(d.Lpad * w_stride(d.QCpad) * 8);
@@ -77,8 +105,97 @@ __host__ __device__ inline SmemLayout smem_layout(const Dims& d, int nbuf) {
   // m_run, S_run, colm, collogS, eta (QCpad each), fac[2][QCpad]; obj_run (RC), hobj (4·RC)
   s.col_off = off;
   off += align16((7 * d.QCpad + 5 * d.RC) * 8);
+  s.tab_off = off;  // 2^(i/64) table of exp_nonpos
+  off += 64 * 8;
+  s.mbar_off = off;  // full[3], empty[3] mbarriers of the X ring
+  off += 6 * 8;
   s.total = off;
   return s;
+}
+
+
+// ---- exp for non-positive arguments (softmax weights), ~1 ulp -------------------
+// x = (k/64)·ln2 + r, |r| ≤ ln2/128:  e^x = 2^⌊k/64⌋ · 2^{(k mod 64)/64} · e^r, with the 64
+// table entries correctly rounded (generated with 60-digit decimal arithmetic), a
+// Cody–Waite split of ln2/64 (hi has 33 significant bits, so k·hi is exact for
+// |k| < 2^17) and a degree-6 Taylor polynomial (truncation < 3e-20).  About half
+// the fp64-pipe instructions of the libdevice exp, which matters because these
+// scalar fp64 ops share the pipe with the DMMA contractions.
+__constant__ double kExp2Tab64[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+__device__ __forceinline__ void load_exp_table(double* T, int tid) {
+  if (tid < 64) T[tid] = kExp2Tab64[tid];
+}
+
+__device__ __forceinline__ double exp_nonpos(double x, const double* T) {
+  if (!(x > -745.0)) return (x == x) ? 0.0 : x;  // −inf and underflow → 0; NaN stays NaN
+  const double kd = rint(x * 92.33248261689366);   // 64 / ln2
+  const int k = static_cast<int>(kd);
+  double r = fma(kd, -0.010830424695086549, x);    // ln2/64, high part
+  r = fma(kd, -1.162596423439437e-12, r);          // ln2/64, low part
+  double q = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  const double y = q * T[k & 63];
+  const int e = k >> 6;  // floor(k / 64)
+  if (e >= -1020) return y * __hiloint2double((e + 1023) << 20, 0);
+  return ldexp(y, e);
+}
+
+// ---- mbarrier + TMA (cp.async.bulk.tensor) ----------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void bar_sync(int id, int n) {

@@ -54,6 +54,7 @@ struct Dims {
   int K1;
   int nbuf;   // X tile buffers in shared memory (2 = prefetch next tile)
   int xbytes; // 4: fp32 image, 8: fp64 image (inputs not exactly representable in fp32)
+  int ncta;   // persistent pass CTAs (one per SM)
 };
 
 struct PassArgs {
@@ -76,6 +77,9 @@ struct PassArgs {
   double* part_obj;       // [nslices][M]
   unsigned long long* fail_key;  // [M]  min over (t<<1 | block)
   double* observe_A;      // optional [K1][p][Npad] inner iterates (M == 1 observed mode)
+  unsigned long long* kprof;  // optional cycle accounting (development)
+  int dbg;                    // development switches (EDAA_DBG): 1 no DMMA, 2 no B update
+  const void* xmap;           // host pointer to the CUtensorMap of X (passed by value at launch)
 };
 
 struct CombineArgs {

@@ -23,8 +23,11 @@
 //   step sizes         solver.cpp:138-149, matrix.cpp:150-190
 //   fit / coherence    ensemble.cpp:29-60; selection ensemble.cpp:71-94
 #pragma once
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+
+#include <cuda.h>
 
 #include "edaa_device.cuh"
 
@@ -58,28 +61,41 @@ struct LanesPerPixel {
   static constexpr int value = PT <= 4 ? 1 : (PT <= 8 ? 2 : 4);
 };
 
-template <int PT, int TPP, bool UPDATE>
+template <int PT, int TPP, bool UPDATE, bool EXACT>
 __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int rl, int j, int pix,
                                                  bool valid, int sub, double* ss, const double* sh,
-                                                 const double* st, const double* gs) {
+                                                 const double* st, const double* gs, const double* T) {
+  // EXACT: p == PT, so every index below is compile-time except the lane's `sub`.
   constexpr int EPT = (PT + TPP - 1) / TPP;
+  constexpr bool kAllValid = EXACT && (PT % TPP == 0);
+  constexpr bool kGinRegs = EXACT && EPT * PT <= 48;  // the lane's rows of G stay in registers
   const Dims& d = pa.d;
-  const int p = d.p;
+  const int p = EXACT ? PT : d.p;
   const int gbase = (threadIdx.x & 31) - sub;
+  const double xn = valid ? pa.xnorm[pix] : 0.0;
+  const double eta = pa.eta_a[r];
   double a[EPT], P[EPT];
+  bool own[EPT];
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const int i = sub * EPT + e;
+    own[e] = kAllValid || i < p;
     a[e] = 0.0;
     P[e] = 0.0;
-    if (i < p) {
+    if (own[e]) {
       const int c = rl * p + i;
       a[e] = st[c * kNP + j];
       P[e] = ss[c * kSST + j] + sh[c * kSST + j];
     }
   }
   const double* G = gs + rl * p * p;
-  const double eta = pa.eta_a[r];
+  double Gr[kGinRegs ? EPT : 1][kGinRegs ? PT : 1];
+  if constexpr (kGinRegs) {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+#pragma unroll
+      for (int m = 0; m < PT; ++m) Gr[e][m] = own[e] ? G[(sub * EPT + e) * PT + m] : 0.0;
+  }
   double aPa = 0.0, aGa = 0.0;
   bool bad = false;
   const int steps = UPDATE ? d.K1 : 1;
@@ -89,12 +105,15 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     for (int e = 0; e < EPT; ++e) ga[e] = 0.0;
 #pragma unroll
     for (int m = 0; m < PT; ++m) {
-      if (m < p) {
+      if (EXACT || m < p) {
         const double am = (TPP == 1) ? a[m % EPT] : __shfl_sync(0xffffffffu, a[m % EPT], gbase + m / EPT);
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
-          const int i = sub * EPT + e;
-          if (i < p) ga[e] += G[i * p + m] * am;
+          if constexpr (kGinRegs) {
+            ga[e] = fma(Gr[e][m], am, ga[e]);
+          } else {
+            if (own[e]) ga[e] += G[(sub * EPT + e) * p + m] * am;
+          }
         }
       }
     }
@@ -103,7 +122,7 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       u[e] = -INFINITY;
-      if (sub * EPT + e < p) {
+      if (own[e]) {
         if (k == 0) {
           aPa += a[e] * P[e];
           aGa += a[e] * ga[e];
@@ -118,9 +137,9 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     double total = 0.0;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      if (sub * EPT + e < p) {
+      if (own[e]) {
         const double z = (a[e] < kLogFloorValue) ? kLogFloorValue : a[e];  // std::max(z, 1e-30)
-        a[e] = z * exp(u[e] - umax);
+        a[e] = z * exp_nonpos(u[e] - umax, T);
         total += a[e];
       }
     }
@@ -129,13 +148,15 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     const double inv = 1.0 / total;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      const int i = sub * EPT + e;
-      if (i < p) {
+      if (own[e]) {
         a[e] *= inv;
         bad |= !isfinite(a[e]);
-        if (pa.observe_A != nullptr && valid)
-          pa.observe_A[(static_cast<size_t>(k) * p + i) * d.Npad + pix] = a[e];
       }
+    }
+    if (pa.observe_A != nullptr && valid) {
+#pragma unroll
+      for (int e = 0; e < EPT; ++e)
+        if (own[e]) pa.observe_A[(static_cast<size_t>(k) * p + sub * EPT + e) * d.Npad + pix] = a[e];
     }
   }
 #pragma unroll
@@ -148,15 +169,15 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     const size_t base = static_cast<size_t>(r) * p * d.Npad + pix;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      const int i = sub * EPT + e;
-      if (i < p) {
+      if (own[e]) {
+        const int i = sub * EPT + e;
         if (valid) pa.A[base + static_cast<size_t>(i) * d.Npad] = a[e];
         ss[(rl * p + i) * kSST + j] = valid ? a[e] : 0.0;
       }
     }
   }
   // ½‖x − Ya‖² ≥ 0; the expanded form can round a few ulps below an exact zero.
-  return (valid && sub == 0) ? fmax(0.5 * ((pa.xnorm[pix] - 2.0 * aPa) + aGa), 0.0) : 0.0;
+  return (valid && sub == 0) ? fmax(0.5 * ((xn - 2.0 * aPa) + aGa), 0.0) : 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -174,13 +195,34 @@ namespace bars {
 constexpr int kS = 1, kW = 3, kMma = 5, kUpd = 6;
 }
 
-// P3 for a warp owning R row tiles (gwarp + 8·i): C[l][c] += Σ_j X[l][j]·w[c][j]
-// over the tile's 32 pixels; pseudo rows ≥ Lpad read w itself (AAᵀ).  R and the
-// three column tiles are compile-time, so the DMMAs are unpredicated.
-template <int R, int RTW, class XT>
+// Optional cycle accounting (PassArgs::kprof != nullptr, development only):
+// warp 0 of each group adds the cycles of its phases into kprof[slot].
+#define EDAA_TSTART() const long long t0_ = (pa.kprof && (lane == 0) && (gwarp == 0)) ? clock64() : 0
+#define EDAA_TSTOP(slot)                                                        \
+  do {                                                                          \
+    if (pa.kprof && lane == 0 && gwarp == 0)                                    \
+      atomicAdd(pa.kprof + 6 * MODE + (slot), static_cast<unsigned long long>(clock64() - t0_)); \
+  } while (0)
+
+// Row stride of the swizzled X tile in elements (one 128-byte smem row).
+template <class XT>
+constexpr int kXRow = 128 / sizeof(XT);
+
+// P3 for a warp owning R X row tiles (gwarp + 8·i, i < R) and, when PSEUDO, one
+// more row tile of pseudo-bands (rows ≥ Lpad read w itself: AAᵀ):
+// C[l][c] += Σ_j X[l][j]·w[c][j] over the tile's 32 pixels.  Row tiles, column
+// tiles and k-steps are compile-time, so the DMMAs are unpredicated and the
+// swizzled X addresses reduce to a per-k-step table (row & 7 == g for every
+// fragment row).
+template <int R, bool PSEUDO, int RTW, class XT>
 __device__ __forceinline__ void accumulate_tiles(double (&ac)[RTW][kMaxCT][2], const XT* xs,
-                                                 const double* w, int gwarp, int nRTx, int g, int t4) {
+                                                 const double* w, int gwarp, int nRTx, int g, int t4,
+                                                 int xrows) {
+  int xo[kNP / 4];
+#pragma unroll
+  for (int kk = 0; kk < kNP / 4; ++kk) xo[kk] = xoff<XT>(g, kk * 4 + t4, xrows);
   const double* wrow = w + g * kSST + t4;
+  const double* prow = w + ((gwarp + 8 * R - nRTx) * 8 + g) * kSST + t4;  // the pseudo tile's rows
 #pragma unroll
   for (int kk = 0; kk < kNP / 4; ++kk) {
     double bw[kMaxCT];
@@ -188,31 +230,22 @@ __device__ __forceinline__ void accumulate_tiles(double (&ac)[RTW][kMaxCT][2], c
     for (int ct = 0; ct < kMaxCT; ++ct) bw[ct] = wrow[ct * 8 * kSST + kk * 4];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const int rt = gwarp + 8 * i;
-      const double ax = (rt < nRTx) ? static_cast<double>(xs[(rt * 8 + g) * kXST + kk * 4 + t4])
-                                    : w[((rt - nRTx) * 8 + g) * kSST + kk * 4 + t4];
+      const double ax = static_cast<double>(xs[(gwarp + 8 * i) * 8 * kXRow<XT> + xo[kk]]);
 #pragma unroll
       for (int ct = 0; ct < kMaxCT; ++ct) dmma(ac[i][ct], ax, bw[ct]);
     }
+    if constexpr (PSEUDO) {
+      const double ax = prow[kk * 4];
+#pragma unroll
+      for (int ct = 0; ct < kMaxCT; ++ct) dmma(ac[R][ct], ax, bw[ct]);
+    }
   }
-}
-
-template <int MODE, class XT>
-__device__ __forceinline__ void issue_x(const PassArgs& pa, XT* xs, int j0, int gtid) {
-  const Dims& d = pa.d;
-  constexpr int kV = 16 / sizeof(XT);  // elements per 16-byte copy
-  const XT* X = static_cast<const XT*>(pa.X);
-  for (int e = gtid; e < d.L * (kNP / kV); e += kGroup) {
-    const int l = e / (kNP / kV), q = e % (kNP / kV);
-    cp_async16(xs + l * kXST + q * kV, X + static_cast<size_t>(l) * d.Npad + j0 + q * kV);
-  }
-  cp_async_commit();
 }
 
 template <int MODE>
 __device__ __forceinline__ void issue_state(const PassArgs& pa, double* st, int j0, int row0,
                                             int nrows, int gtid) {
-  if (MODE != kModeInit) {
+  if (MODE != kModeInit && !(pa.dbg & 8)) {
     const double* src = (MODE == kModeB) ? pa.Lg : pa.A;
     for (int e = gtid; e < nrows * (kNP / 2); e += kGroup) {
       const int c = e / (kNP / 2), q = e % (kNP / 2);
@@ -222,8 +255,46 @@ __device__ __forceinline__ void issue_state(const PassArgs& pa, double* st, int 
   cp_async_commit();
 }
 
+// Work decomposition: item k (0 ≤ k < NCH·nslices) is (slice k / NCH, chunk
+// k % NCH) — slice-major, so a CTA sweeps the run chunks over the same pixel
+// slice back to back and X is re-read from L2, not HBM; persistent CTA b of G
+// processes items [b·K/G, (b+1)·K/G) as ONE flattened stream of 32-pixel
+// tiles (the pipeline never drains between items), restaging the W chunk and
+// the per-column constants when the chunk changes and flushing every item's
+// partials when its last tile retires.
+struct Cursor {
+  int item, tile, tend;
+};
+
+__device__ __forceinline__ int slice_tile(const Dims& d, int s) {
+  return static_cast<int>((static_cast<long long>(s) * d.ntiles) / d.nslices);
+}
+__device__ __forceinline__ void cursor_set(Cursor& c, const Dims& d, int item) {
+  const int s = item / d.NCH;
+  c.item = item;
+  c.tile = slice_tile(d, s);
+  c.tend = slice_tile(d, s + 1);
+}
+__device__ __forceinline__ void cursor_next(Cursor& c, const Dims& d) {
+  if (++c.tile == c.tend) cursor_set(c, d, c.item + 1);
+}
+
+struct ChunkInfo {
+  int chunk, run0, RCe, ncol, col0, srow0;
+};
+__device__ __forceinline__ ChunkInfo chunk_info(const Dims& d, int item) {
+  ChunkInfo ci;
+  ci.chunk = item % d.NCH;
+  ci.run0 = ci.chunk * d.RC;
+  ci.RCe = min(d.RC, d.M - ci.run0);
+  ci.ncol = ci.RCe * d.p;
+  ci.col0 = ci.chunk * d.QCpad;
+  ci.srow0 = ci.run0 * d.p;
+  return ci;
+}
+
 template <int MODE, int PT, int RTW, class XT>
-__global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
+__global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Dims& d = pa.d;
   const int nbuf = d.nbuf;
@@ -234,10 +305,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
   double* S_run = m_run + d.QCpad;
   double* c_m = S_run + d.QCpad;      // normaliser max of the previous logits (B pass)
   double* c_logS = c_m + d.QCpad;     // its log-sum
-  double* c_eta = c_logS + d.QCpad;   // η of the column's run (η_b for B, η_a for A)
+  double* c_eta = c_logS + d.QCpad;   // η_b of the column's run (B pass)
   double* facb = c_eta + d.QCpad;     // [2][QCpad] running-max rescale of tile i%2
   double* obj_run = facb + 2 * d.QCpad;
   double* hobj = obj_run + d.RC;
+  double* etab = reinterpret_cast<double*>(smem + lay.tab_off);
   auto xbuf = [&](int i) { return reinterpret_cast<XT*>(smem + lay.xs_off + (i % nbuf) * lay.xs_bytes); };
   auto sbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.ss_off + (i & 1) * lay.buf_bytes); };
   auto hbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.sh_off + (i & 1) * lay.buf_bytes); };
@@ -248,58 +320,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
   const int gtid = tid & (kGroup - 1);
   const int lane = tid & 31, gwarp = gtid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int slice = blockIdx.x;
-  const int chunk = blockIdx.y;
   const int p = d.p;
-  const int run0 = chunk * d.RC;
-  const int RCe = min(d.RC, d.M - run0);  // runs present in this chunk
-  const int ncol_valid = RCe * p;
   const int nRTx = d.Lpad / 8;
   const int nRT = (MODE == kModeA) ? nRTx + d.QCpad / 8 : nRTx;
   const int WST = w_stride(d.QCpad);
-  const int col0 = chunk * d.QCpad;
-  const int srow0 = run0 * p;  // first state row (A / Lg) of this chunk
 
-  const int tile_begin = static_cast<int>((static_cast<long long>(slice) * d.ntiles) / d.nslices);
-  const int tile_end = static_cast<int>((static_cast<long long>(slice + 1) * d.ntiles) / d.nslices);
-  const int ntile = tile_end - tile_begin;
+  const int K = d.NCH * d.nslices;
+  const int item_begin = static_cast<int>((static_cast<long long>(blockIdx.x) * K) / gridDim.x);
+  const int item_end = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * K) / gridDim.x);
+  int ntile = 0;
+  for (int k = item_begin; k < item_end; ++k) {
+    const int s = k / d.NCH;
+    ntile += slice_tile(d, s + 1) - slice_tile(d, s);
+  }
+  if (ntile == 0) return;
 
-  // First tiles in flight while the constants are staged.
-  if (mma_group) {
-    issue_x<MODE, XT>(pa, xbuf(0), tile_begin * kNP, gtid);
-    if (ntile > 1) issue_x<MODE, XT>(pa, xbuf(1), (tile_begin + 1) * kNP, gtid);
-  } else {
-    issue_state<MODE>(pa, stbuf(0), tile_begin * kNP, srow0, ncol_valid, gtid);
-  }
-  // ---- one-time staging (all 512 threads) ----
-  if (MODE != kModeInit) {
-    for (int e = tid; e < d.Lpad * d.QCpad; e += kThreads) {
-      const int l = e / d.QCpad, c = e % d.QCpad;
-      ws[l * WST + c] = pa.W[static_cast<size_t>(l) * d.Qs + col0 + c];
+  // ---- one-time setup (all 512 threads) ----
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + lay.mbar_off);
+  unsigned long long* empty = full + 3;
+  if (tid == 0) {
+    for (int b = 0; b < nbuf; ++b) {
+      mbar_init(full + b, 1);   // the producer's arrive.expect_tx; TMA completes the bytes
+      mbar_init(empty + b, 8);  // one arrive per MMA warp after its last read of the tile
     }
+    mbar_fence_init();
   }
-  if (MODE == kModeA || MODE == kModeObj) {
-    for (int e = tid; e < RCe * p * p; e += kThreads) {
-      const int rl = e / (p * p), rem = e % (p * p);
-      const int i = rem / p, m = rem % p;
-      gs[e] = pa.Gbuf[static_cast<size_t>(rl * p + i) * d.Qs + col0 + rl * p + m];
-    }
-  }
-  for (int b = 0; b < nbuf; ++b)
-    for (int e = tid; e < (d.Lpad - d.L) * kNP; e += kThreads)
-      xbuf(b)[(d.L + e / kNP) * kXST + e % kNP] = XT(0);
-  if (tid < d.QCpad) {
-    const int c = tid;
-    m_run[c] = -INFINITY;
-    S_run[c] = 0.0;
-    facb[c] = facb[d.QCpad + c] = 1.0;
-    const bool real = c < ncol_valid;
-    const int r = run0 + (real ? c / p : 0);
-    c_m[c] = (MODE == kModeB && real) ? pa.colm[col0 + c] : 0.0;
-    c_logS[c] = (MODE == kModeB && real) ? pa.collogS[col0 + c] : 0.0;
-    c_eta[c] = real ? (MODE == kModeB ? pa.eta_b[r] : (MODE == kModeInit ? 0.0 : pa.eta_a[r])) : 0.0;
-  }
-  if (tid < d.RC) obj_run[tid] = 0.0;
+  if (tid < d.QCpad) facb[tid] = facb[d.QCpad + tid] = 1.0;
+  load_exp_table(etab, tid);
   __syncthreads();
 
   if (mma_group) {
@@ -309,110 +356,226 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
     for (int i = 0; i < RTW; ++i)
 #pragma unroll
       for (int c = 0; c < kMaxCT; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
+    const int my_rt = (nRT - gwarp + 7) / 8;  // row tiles gwarp + 8·i < nRT
+    const int my_x = (nRTx - gwarp + 7) / 8;  // of which X rows (the rest: one pseudo tile)
+    const bool my_pseudo = my_rt > my_x;
+    Cursor xc, p1c, p3c;
+    cursor_set(xc, d, item_begin);
+    cursor_set(p1c, d, item_begin);
+    cursor_set(p3c, d, item_begin);
+    int wchunk = -1;
 
-    // row tiles owned by this warp: gwarp + 8·i < nRT
-    const int my_rt = (nRT - gwarp + 7) / 8;
-    // P1(i): S[c][j] = Σ_l W[l][c]·X[l][j]; warp = 8 pixels × one band half.
-    auto phase1 = [&](int i) {
-      if (MODE != kModeInit) {
-        const XT* xs = xbuf(i);
-        const int pt = gwarp & 3, half = gwarp >> 2;
-        const int kh = d.Lpad / 8;  // k-steps per band half
-        double c1[kMaxCT][2];
-#pragma unroll
-        for (int c = 0; c < kMaxCT; ++c) c1[c][0] = c1[c][1] = 0.0;
-        const XT* xcol = xs + pt * 8 + g;
-        const double* wcol = ws + g;
-#pragma unroll 4
-        for (int kk = half * kh; kk < (half + 1) * kh; ++kk) {
-          const int l = kk * 4 + t4;
-          const double bx = static_cast<double>(xcol[l * kXST]);
-#pragma unroll
-          for (int ct = 0; ct < kMaxCT; ++ct) dmma(c1[ct], wcol[l * WST + ct * 8], bx);
-        }
-        double* dst = half ? hbuf(i) : sbuf(i);
-#pragma unroll
-        for (int ct = 0; ct < kMaxCT; ++ct)
-          *reinterpret_cast<double2*>(dst + (ct * 8 + g) * kSST + pt * 8 + 2 * t4) =
-              make_double2(c1[ct][0], c1[ct][1]);
+    const int xrows = x_rows(d), brows = x_box_rows(d);
+    const int nbox = xrows / brows, nhalf = sizeof(XT) / 4;  // row boxes × column halves
+    const unsigned tile_tx = static_cast<unsigned>(nbox * nhalf * brows * 128);
+    // Producer (MMA thread 0): X(f) into slot f % nbuf once the slot's previous
+    // tile has been released by all 8 MMA warps (empty barrier).
+    auto load_next_x = [&](int f) {
+      if (gtid == 0) {
+        const int b = f % nbuf, u = f / nbuf;
+        if (u > 0) mbar_wait(empty + b, (u - 1) & 1);
+        mbar_expect_tx(full + b, tile_tx);
+        XT* dst = xbuf(f);
+        for (int h = 0; h < nhalf; ++h)
+          for (int bx = 0; bx < nbox; ++bx)
+            tma_load_2d(dst + h * xrows * (32 / nhalf) + bx * brows * (32 / nhalf), &xmap,
+                        xc.tile * kNP + h * 16, bx * brows, full + b);
       }
+      cursor_next(xc, d);
     };
-    // wait for X(i) (the only other group in flight may be X(i+1)), publish to the group
-    auto x_ready = [&](int i, bool newer_in_flight) {
-      if (newer_in_flight) cp_async_wait1(); else cp_async_wait0();
-      bar_sync(bars::kMma, kGroup);
+    auto x_wait = [&](int i) { mbar_wait(full + i % nbuf, (i / nbuf) & 1); };
+    auto x_release = [&](int i) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + i % nbuf);
+    };
+    // P1: S[c][j] = Σ_l W[l][c]·X[l][j]; warp = 8 pixels × one band half.
+    auto phase1 = [&](int i) {
+      if (MODE == kModeInit || (pa.dbg & 1)) return;
+      const int chunk = p1c.item % d.NCH;
+      if (chunk != wchunk) {  // restage W once every MMA warp is past its previous P1
+        bar_sync(bars::kMma, kGroup);
+        for (int e = gtid; e < d.Lpad * d.QCpad; e += kGroup) {
+          const int l = e / d.QCpad, c = e % d.QCpad;
+          ws[l * WST + c] = pa.W[static_cast<size_t>(l) * d.Qs + chunk * d.QCpad + c];
+        }
+        bar_sync(bars::kMma, kGroup);
+        wchunk = chunk;
+      }
+      const XT* xs = xbuf(i);
+      const int pt = gwarp & 3, half = gwarp >> 2;
+      double c1[kMaxCT][2];
+#pragma unroll
+      for (int c = 0; c < kMaxCT; ++c) c1[c][0] = c1[c][1] = 0.0;
+      const double* wcol = ws + t4 * WST + g;
+      // X[l][pt·8+g], l = kk·4 + t4: (l & 7) depends only on the parity of kk
+      const int xo0 = xoff<XT>(t4, pt * 8 + g, xrows), xo1 = xoff<XT>(4 + t4, pt * 8 + g, xrows);
+      // band halves of even length: K4 = Lpad/4 k-steps is even, split at h0 = 2⌊K4/4⌋
+      const int h0 = 2 * (d.Lpad / 16);
+      const int kb = half ? h0 : 0;
+      const int kn = half ? d.Lpad / 4 - h0 : h0;
+#pragma unroll 2
+      for (int k2 = 0; k2 < kn / 2; ++k2) {
+        const int kk = kb + 2 * k2;
+        const XT* xr = xs + (kk >> 1) * 8 * kXRow<XT>;
+        const double bx0 = static_cast<double>(xr[xo0]);
+        const double bx1 = static_cast<double>(xr[xo1]);
+        const double* w0 = wcol + kk * 4 * WST;
+        const double* w1 = w0 + 4 * WST;
+#pragma unroll
+        for (int ct = 0; ct < kMaxCT; ++ct) dmma(c1[ct], w0[ct * 8], bx0);
+#pragma unroll
+        for (int ct = 0; ct < kMaxCT; ++ct) dmma(c1[ct], w1[ct * 8], bx1);
+      }
+      double* dst = half ? hbuf(i) : sbuf(i);
+#pragma unroll
+      for (int ct = 0; ct < kMaxCT; ++ct)
+        *reinterpret_cast<double2*>(dst + (ct * 8 + g) * kSST + pt * 8 + 2 * t4) =
+            make_double2(c1[ct][0], c1[ct][1]);
     };
 
-    x_ready(0, ntile > 1);
+    load_next_x(0);
+    if (ntile > 1) load_next_x(1);
+    x_wait(0);
     phase1(0);
+    cursor_next(p1c, d);
     bar_arrive(bars::kS + 0, kThreads);
     for (int it = 0; it < ntile; ++it) {
       if (it + 1 < ntile) {
-        x_ready(it + 1, false);
-        // three buffers: X(i+2) goes into X(i−1)'s slot, free since the barrier above
-        if (nbuf > 2 && it + 2 < ntile) issue_x<MODE, XT>(pa, xbuf(it + 2), (tile_begin + it + 2) * kNP, gtid);
-        phase1(it + 1);
+        {
+          EDAA_TSTART();
+          x_wait(it + 1);
+          EDAA_TSTOP(0);
+        }
+        {
+          EDAA_TSTART();
+          phase1(it + 1);
+          EDAA_TSTOP(1);
+        }
+        // three slots: X(i+2) reuses X(i−1)'s slot, released after P3(i−1)
+        if (nbuf > 2 && it + 2 < ntile) load_next_x(it + 2);
+        cursor_next(p1c, d);
         bar_arrive(bars::kS + ((it + 1) & 1), kThreads);
       }
-      bar_sync(bars::kW + (it & 1), kThreads);  // w(i), fac(i) ready
+      {
+        EDAA_TSTART();
+        bar_sync(bars::kW + (it & 1), kThreads);  // w(i), fac(i) ready
+        EDAA_TSTOP(2);
+      }
       if (MODE != kModeObj) {
-      const double* fac = facb + (it & 1) * d.QCpad;
-      if (MODE == kModeB || MODE == kModeInit) {
+        if (MODE == kModeB || MODE == kModeInit) {
+          const double* fac = facb + (it & 1) * d.QCpad;
 #pragma unroll
-        for (int ct = 0; ct < kMaxCT; ++ct) {
-          const double f0 = fac[ct * 8 + 2 * t4], f1 = fac[ct * 8 + 2 * t4 + 1];
-          if (f0 != 1.0 || f1 != 1.0) {
+          for (int ct = 0; ct < kMaxCT; ++ct) {
+            const double f0 = fac[ct * 8 + 2 * t4], f1 = fac[ct * 8 + 2 * t4 + 1];
+            if (f0 != 1.0 || f1 != 1.0) {
 #pragma unroll
-            for (int i = 0; i < RTW; ++i) {
-              acc[i][ct][0] *= f0;
-              acc[i][ct][1] *= f1;
+              for (int i = 0; i < RTW; ++i) {
+                acc[i][ct][0] *= f0;
+                acc[i][ct][1] *= f1;
+              }
             }
           }
         }
-      }
-      // P3(i): C[l][c] += Σ_j X[l][j]·w[c][j]; warp owns row tiles gwarp, gwarp+8, …
-      const XT* xs = xbuf(it);
-      const double* w = sbuf(it);
-      switch (my_rt) {  // warp-uniform: the DMMAs below are unpredicated
-        case 1: accumulate_tiles<1>(acc, xs, w, gwarp, nRTx, g, t4); break;
-        case 2: accumulate_tiles<2>(acc, xs, w, gwarp, nRTx, g, t4); break;
-        case 3: accumulate_tiles<3>(acc, xs, w, gwarp, nRTx, g, t4); break;
-        case 4: if constexpr (RTW >= 4) accumulate_tiles<4>(acc, xs, w, gwarp, nRTx, g, t4); break;
-        case 5: if constexpr (RTW >= 5) accumulate_tiles<5>(acc, xs, w, gwarp, nRTx, g, t4); break;
-        case 6: if constexpr (RTW >= 6) accumulate_tiles<6>(acc, xs, w, gwarp, nRTx, g, t4); break;
-        default: break;
-      }
-      }  // MODE != kModeObj
-      if (nbuf == 2 && it + 2 < ntile) {  // X(i) is consumed: reuse its buffer for X(i+2)
-        bar_sync(bars::kMma, kGroup);
-        issue_x<MODE, XT>(pa, xbuf(it + 2), (tile_begin + it + 2) * kNP, gtid);
-      }
-    }
-    if (MODE != kModeObj) {
+        // P3: C[l][c] += Σ_j X[l][j]·w[c][j]; warp owns row tiles gwarp, gwarp+8, …
+        const XT* xs = xbuf(it);
+        const double* w = sbuf(it);
+        EDAA_TSTART();
+        if (!(pa.dbg & 1)) {
+          switch (my_x + (my_pseudo ? 8 : 0)) {  // warp-uniform: the DMMAs below are unpredicated
+            case 1: accumulate_tiles<1, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 2: accumulate_tiles<2, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 3: accumulate_tiles<3, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 4: if constexpr (RTW >= 4) accumulate_tiles<4, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 5: if constexpr (RTW >= 5) accumulate_tiles<5, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 6: if constexpr (RTW >= 6) accumulate_tiles<6, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 8: if constexpr (MODE == kModeA) accumulate_tiles<0, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 9: if constexpr (MODE == kModeA) accumulate_tiles<1, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 10: if constexpr (MODE == kModeA) accumulate_tiles<2, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 11: if constexpr (MODE == kModeA) accumulate_tiles<3, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 12: if constexpr (MODE == kModeA && RTW >= 5) accumulate_tiles<4, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 13: if constexpr (MODE == kModeA && RTW >= 6) accumulate_tiles<5, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            default: break;
+          }
+        }
+        EDAA_TSTOP(3);
+        if (p3c.tile + 1 == p3c.tend) {  // the item's last tile: flush and restart its partials
+          const int slice = p3c.item / d.NCH, col0 = (p3c.item % d.NCH) * d.QCpad;
 #pragma unroll
-      for (int i = 0; i < RTW; ++i) {
-        const int rt = gwarp + 8 * i;
-        if (rt < nRT) {
-          const int row = rt * 8 + g;
+          for (int i = 0; i < RTW; ++i) {
+            const int rt = gwarp + 8 * i;
+            if (rt < nRT) {
+              const int row = rt * 8 + g;
 #pragma unroll
-          for (int ct = 0; ct < kMaxCT; ++ct) {
-            double* dst = pa.part_C + (static_cast<size_t>(slice) * d.Lrows + row) * d.Qs + col0 +
-                          ct * 8 + 2 * t4;
-            *reinterpret_cast<double2*>(dst) = make_double2(acc[i][ct][0], acc[i][ct][1]);
+              for (int ct = 0; ct < kMaxCT; ++ct) {
+                double* dst = pa.part_C + (static_cast<size_t>(slice) * d.Lrows + row) * d.Qs + col0 +
+                              ct * 8 + 2 * t4;
+                *reinterpret_cast<double2*>(dst) = make_double2(acc[i][ct][0], acc[i][ct][1]);
+              }
+            }
+#pragma unroll
+            for (int ct = 0; ct < kMaxCT; ++ct) acc[i][ct][0] = acc[i][ct][1] = 0.0;
           }
         }
       }
+      x_release(it);  // this warp is done with X(i) (P1(i) and P3(i))
+      cursor_next(p3c, d);
+      if (nbuf == 2 && it + 2 < ntile) load_next_x(it + 2);  // two slots: reuse X(i)'s
     }
   } else {
     // ========================== update group ==========================
+    Cursor sc, p2c;
+    cursor_set(sc, d, item_begin);
+    cursor_set(p2c, d, item_begin);
+    int cchunk = -1;
+    {
+      const ChunkInfo ci = chunk_info(d, sc.item);
+      issue_state<MODE>(pa, stbuf(0), sc.tile * kNP, ci.srow0, ci.ncol, gtid);
+      cursor_next(sc, d);
+    }
     for (int it = 0; it < ntile; ++it) {
-      const int j0 = (tile_begin + it) * kNP;
-      bar_sync(bars::kUpd, kGroup);  // everyone is done with st(i−1)
+      const ChunkInfo ci = chunk_info(d, p2c.item);
+      const int j0 = p2c.tile * kNP;
+      const bool item_first = p2c.tile == slice_tile(d, p2c.item / d.NCH);
+      const bool item_last = p2c.tile + 1 == p2c.tend;
+      bar_sync(bars::kUpd, kGroup);  // everyone is done with st(i−1) and the previous item's scalars
       const bool more = it + 1 < ntile;
-      if (more) issue_state<MODE>(pa, stbuf(it + 1), j0 + kNP, srow0, ncol_valid, gtid);
+      if (more) {
+        const ChunkInfo cn = chunk_info(d, sc.item);
+        issue_state<MODE>(pa, stbuf(it + 1), sc.tile * kNP, cn.srow0, cn.ncol, gtid);
+        cursor_next(sc, d);
+      }
+      if (ci.chunk != cchunk) {  // per-column constants and G blocks of the new chunk
+        if (gtid < d.QCpad) {
+          const int c = gtid;
+          const bool real = c < ci.ncol;
+          c_m[c] = (MODE == kModeB && real) ? pa.colm[ci.col0 + c] : 0.0;
+          c_logS[c] = (MODE == kModeB && real) ? pa.collogS[ci.col0 + c] : 0.0;
+          c_eta[c] = (MODE == kModeB && real) ? pa.eta_b[ci.run0 + c / p] : 0.0;
+        }
+        if (MODE == kModeA || MODE == kModeObj) {
+          for (int e = gtid; e < ci.RCe * p * p; e += kGroup) {
+            const int rl = e / (p * p), rem = e % (p * p);
+            const int i = rem / p, m = rem % p;
+            gs[e] = pa.Gbuf[static_cast<size_t>(rl * p + i) * d.Qs + ci.col0 + rl * p + m];
+          }
+        }
+        cchunk = ci.chunk;
+      }
+      if (item_first) {
+        if (gtid < d.QCpad) {
+          m_run[gtid] = -INFINITY;
+          S_run[gtid] = 0.0;
+        }
+        if (gtid < d.RC) obj_run[gtid] = 0.0;
+      }
       if (more) cp_async_wait1(); else cp_async_wait0();
-      bar_sync(bars::kUpd, kGroup);  // st(i) visible
-      bar_sync(bars::kS + (it & 1), kThreads);  // S(i) ready
+      bar_sync(bars::kUpd, kGroup);  // st(i), constants and resets visible
+      {
+        EDAA_TSTART();
+        bar_sync(bars::kS + (it & 1), kThreads);  // S(i) ready
+        EDAA_TSTOP(4);
+      }
+      EDAA_TSTART();
       double* ss = sbuf(it);
       const double* sh = hbuf(it);
       const double* st = stbuf(it);
@@ -420,33 +583,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
 
       if (MODE == kModeA || MODE == kModeObj) {
         constexpr int TPP = LanesPerPixel<PT>::value;
-        for (int q2 = gtid; q2 < RCe * kNP * TPP; q2 += kGroup) {  // warp-uniform trip count
+        for (int q2 = gtid; q2 < ci.RCe * kNP * TPP; q2 += kGroup) {  // warp-uniform trip count
           const int q = q2 / TPP, sub = q2 % TPP;
           const int rl = q / kNP, j = q % kNP;
           const int pix = j0 + j;
-          double o = pixel_a_update<PT, TPP, MODE == kModeA>(pa, run0 + rl, rl, j, pix, pix < d.N, sub,
-                                                               ss, sh, st, gs);
+          double o = (p == PT)
+              ? pixel_a_update<PT, TPP, MODE == kModeA, true>(pa, ci.run0 + rl, rl, j, pix, pix < d.N, sub,
+                                                              ss, sh, st, gs, etab)
+              : pixel_a_update<PT, TPP, MODE == kModeA, false>(pa, ci.run0 + rl, rl, j, pix, pix < d.N, sub,
+                                                               ss, sh, st, gs, etab);
           o = warp_sum(o);
           if (lane == 0) hobj[q2 >> 5] = o;  // warp-task q2/32 belongs to run (q2/32)/TPP
         }
         if (MODE == kModeA)
-          for (int e = gtid; e < (d.QCpad - ncol_valid) * kNP; e += kGroup)
-            ss[(ncol_valid + e / kNP) * kSST + e % kNP] = 0.0;
+          for (int e = gtid; e < (d.QCpad - ci.ncol) * kNP; e += kGroup)
+            ss[(ci.ncol + e / kNP) * kSST + e % kNP] = 0.0;
         bar_sync(bars::kUpd, kGroup);
-        if (gtid < RCe) {
+        if (gtid < ci.RCe) {
           double o = obj_run[gtid];
           for (int h = 0; h < TPP; ++h) o += hobj[gtid * TPP + h];
           obj_run[gtid] = o;
         }
-      } else {
+      } else if (!(pa.dbg & 2)) {
         // B step / B⁰: new logits; 8 lanes per column, 4 pixels per lane (j = k·8 + lane8).
         const int c = gtid >> 3, l8 = gtid & 7;
         const bool active = c < d.QCpad;  // QCpad·8 ≤ 192 threads carry columns
         double ell[4];
         double tmax = -INFINITY;
         if (active) {
-          const bool real = c < ncol_valid;
-          const int rl = real ? c / p : 0, i = real ? c % p : 0, r = run0 + rl;
+          const bool real = c < ci.ncol;
+          const int rl = real ? c / p : 0, i = real ? c % p : 0, r = ci.run0 + rl;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int j = k * 8 + l8, pix = j0 + j;
@@ -461,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
                 lb = (lb < log_floor()) ? log_floor() : lb;                // log max(b, 1e-30)
                 v = lb + (ss[c * kSST + j] + sh[c * kSST + j]) * c_eta[c]; // + η_b·(−∇_B)
               }
-              pa.Lg[static_cast<size_t>(srow0 + c) * d.Npad + pix] = v;
+              pa.Lg[static_cast<size_t>(ci.srow0 + c) * d.Npad + pix] = v;
             }
             ell[k] = v;
             tmax = fmax(tmax, v);
@@ -476,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
           mn = fmax(mo, tmax);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const double w = (mn == -INFINITY) ? 0.0 : exp(ell[k] - mn);
+            const double w = (mn == -INFINITY) ? 0.0 : exp_nonpos(ell[k] - mn, etab);
             ss[c * kSST + k * 8 + l8] = w;
             tsum += w;
           }
@@ -484,31 +650,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa) {
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
         if (active && l8 == 0) {
-          const double f = (mn == -INFINITY || mn == mo) ? 1.0 : exp(mo - mn);
+          const double f = (mn == -INFINITY || mn == mo) ? 1.0 : exp_nonpos(mo - mn, etab);
           fac[c] = f;
           S_run[c] = S_run[c] * f + tsum;
           m_run[c] = mn;
         }
       }
-      bar_arrive(bars::kW + (it & 1), kThreads);  // w(i), fac(i) ready for P3(i)
-    }
-    bar_sync(bars::kUpd, kGroup);
-    if (MODE == kModeB || MODE == kModeInit) {
-      if (gtid < d.QCpad) {
-        pa.part_m[static_cast<size_t>(slice) * d.Qs + col0 + gtid] = m_run[gtid];
-        pa.part_S[static_cast<size_t>(slice) * d.Qs + col0 + gtid] = S_run[gtid];
+      EDAA_TSTOP(5);
+      if (item_last) {  // the item's softmax / objective partials
+        bar_sync(bars::kUpd, kGroup);
+        const int slice = p2c.item / d.NCH;
+        if (MODE == kModeB || MODE == kModeInit) {
+          if (gtid < d.QCpad) {
+            pa.part_m[static_cast<size_t>(slice) * d.Qs + ci.col0 + gtid] = m_run[gtid];
+            pa.part_S[static_cast<size_t>(slice) * d.Qs + ci.col0 + gtid] = S_run[gtid];
+          }
+        } else {
+          if (gtid < ci.RCe) pa.part_obj[static_cast<size_t>(slice) * d.M + ci.run0 + gtid] = obj_run[gtid];
+        }
       }
-    } else {
-      if (gtid < RCe) pa.part_obj[static_cast<size_t>(slice) * d.M + run0 + gtid] = obj_run[gtid];
+      bar_arrive(bars::kW + (it & 1), kThreads);  // w(i), fac(i) ready for P3(i)
+      cursor_next(p2c, d);
     }
   }
 }
 
 template <int MODE, int RTW, class XT>
 cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
-  const dim3 grid(a.d.nslices, a.d.NCH);
+  const dim3 grid(std::min(a.d.NCH * a.d.nslices, a.d.ncta));
   const size_t smem = dev::smem_layout(a.d, a.d.nbuf).total;
-  void (*kern)(PassArgs) = nullptr;
+  void (*kern)(PassArgs, CUtensorMap) = nullptr;
   if (MODE == kModeInit || MODE == kModeB) {
     kern = k_pass<MODE, 1, RTW, XT>;
   } else {
@@ -527,7 +698,7 @@ cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads, smem, st>>>(a);
+  kern<<<grid, kThreads, smem, st>>>(a, *static_cast<const CUtensorMap*>(a.xmap));
   return cudaGetLastError();
 }
 
