@@ -186,7 +186,14 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.Lrows = d.Lpad + d.QCpad;
   d.K1 = static_cast<int>(prm->inner_iters_a);
   d.ncta = c->num_sms;
-  d.nbuf = (edaa::pass_smem_bytes(d, 3) <= static_cast<size_t>(edaa::kMaxSmem)) ? 3 : 2;
+  // Ring depths, as deep as shared memory allows: X tiles (≥ 2) and projection /
+  // weight tiles (≥ 2); the X ring is shortened first.
+  d.nbuf = 4;
+  d.nsb = 2;  // P1(i) reuses w(i−2)'s buffer after the sfree barrier
+  while (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem) && (d.nbuf > 2 || d.nsb > 2)) {
+    if (d.nbuf > 3 || (d.nbuf > 2 && d.nsb == 2)) --d.nbuf;
+    else --d.nsb;
+  }
   if (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem))
     return set_err(c, EDAA_ERR_UNSUPPORTED, "tile working set exceeds shared memory");
   *out = d;

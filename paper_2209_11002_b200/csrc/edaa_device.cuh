@@ -54,8 +54,10 @@ struct SmemLayout {
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 
-// W row stride (doubles): ≡ 8 mod 16 so a DMMA A-fragment (4 rows × 8 columns) hits 2 wavefronts.
-__host__ __device__ inline int w_stride(int qcpad) { return qcpad + ((qcpad % 16 == 0) ? 8 : 0); }
+// W row stride (doubles) ≡ 2 mod 8: the P1 A-fragment reads rows 2 apart (band
+// order of pass P1), 4·stride words ≡ 8 mod 32, so each half-warp's LDS.64 is one
+// conflict-free wavefront.
+__host__ __device__ inline int w_stride(int qcpad) { return qcpad + ((2 - qcpad % 8 + 8) % 8); }
 
 // X tiles arrive by TMA with 128-byte swizzle: each smem row holds 128 bytes
 // (32 floats, or 16 doubles — an fp64 tile is two 16-column halves).  Boxes
@@ -93,13 +95,13 @@ __host__ __device__ inline SmemLayout smem_layout(const Dims& d, int nbuf) {
   s.ws_off = off;
   off += align16(d.Lpad * w_stride(d.QCpad) * 8);
   s.buf_bytes = align16(d.QCpad * kSST * 8);
-  s.ss_off = off;
-  off += 2 * s.buf_bytes;
-  s.sh_off = off;
-  off += 2 * s.buf_bytes;
+  s.ss_off = off;  // nsb buffers of projection half 0 / weights
+  off += d.nsb * s.buf_bytes;
+  s.sh_off = off;  // nsb buffers of projection half 1
+  off += d.nsb * s.buf_bytes;
   s.st_bytes = align16(d.QCpad * kNP * 8);
   s.st_off = off;
-  off += 2 * s.st_bytes;
+  off += 3 * s.st_bytes;  // state tiles i, i+1, i+2 in flight
   s.gs_off = off;
   off += align16(d.RC * d.p * d.p * 8);
   // m_run, S_run, colm, collogS, eta (QCpad each), fac[2][QCpad]; obj_run (RC), hobj (4·RC)
@@ -107,8 +109,8 @@ __host__ __device__ inline SmemLayout smem_layout(const Dims& d, int nbuf) {
   off += align16((7 * d.QCpad + 5 * d.RC) * 8);
   s.tab_off = off;  // 2^(i/64) table of exp_nonpos
   off += 64 * 8;
-  s.mbar_off = off;  // full[3], empty[3] mbarriers of the X ring
-  off += 6 * 8;
+  s.mbar_off = off;  // full[4], empty[4] X ring; sready[2], wready[2] hand-offs; sfree[4]
+  off += 16 * 8;
   s.total = off;
   return s;
 }
@@ -182,6 +184,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -205,6 +220,7 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait2() { asm volatile("cp.async.wait_group 2;\n" ::: "memory"); }
 
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll

@@ -55,6 +55,7 @@ struct Dims {
   int nbuf;   // X tile buffers in shared memory (2 = prefetch next tile)
   int xbytes; // 4: fp32 image, 8: fp64 image (inputs not exactly representable in fp32)
   int ncta;   // persistent pass CTAs (one per SM)
+  int nsb;    // projection/weight tile buffers (2..4)
 };
 
 struct PassArgs {

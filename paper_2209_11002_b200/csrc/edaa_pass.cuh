@@ -263,28 +263,36 @@ __device__ __forceinline__ void issue_state(const PassArgs& pa, double* st, int 
 // the per-column constants when the chunk changes and flushing every item's
 // partials when its last tile retires.
 struct Cursor {
-  int item, tile, tend;
+  int item, slice, chunk, tile, tend;
 };
 
 __device__ __forceinline__ int slice_tile(const Dims& d, int s) {
-  return static_cast<int>((static_cast<long long>(s) * d.ntiles) / d.nslices);
+  return (s * d.ntiles) / d.nslices;  // < 2^31: ntiles ≤ 2^25, nslices ≤ 296
 }
 __device__ __forceinline__ void cursor_set(Cursor& c, const Dims& d, int item) {
-  const int s = item / d.NCH;
   c.item = item;
-  c.tile = slice_tile(d, s);
-  c.tend = slice_tile(d, s + 1);
+  c.slice = item / d.NCH;
+  c.chunk = item - c.slice * d.NCH;
+  c.tile = slice_tile(d, c.slice);
+  c.tend = slice_tile(d, c.slice + 1);
 }
 __device__ __forceinline__ void cursor_next(Cursor& c, const Dims& d) {
-  if (++c.tile == c.tend) cursor_set(c, d, c.item + 1);
+  if (++c.tile != c.tend) return;
+  ++c.item;  // slice-major: the next chunk of the same slice, then the next slice
+  if (++c.chunk == d.NCH) {
+    c.chunk = 0;
+    ++c.slice;
+  }
+  c.tile = slice_tile(d, c.slice);
+  c.tend = slice_tile(d, c.slice + 1);
 }
 
 struct ChunkInfo {
   int chunk, run0, RCe, ncol, col0, srow0;
 };
-__device__ __forceinline__ ChunkInfo chunk_info(const Dims& d, int item) {
+__device__ __forceinline__ ChunkInfo chunk_info(const Dims& d, int chunk) {
   ChunkInfo ci;
-  ci.chunk = item % d.NCH;
+  ci.chunk = chunk;
   ci.run0 = ci.chunk * d.RC;
   ci.RCe = min(d.RC, d.M - ci.run0);
   ci.ncol = ci.RCe * d.p;
@@ -311,9 +319,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   double* hobj = obj_run + d.RC;
   double* etab = reinterpret_cast<double*>(smem + lay.tab_off);
   auto xbuf = [&](int i) { return reinterpret_cast<XT*>(smem + lay.xs_off + (i % nbuf) * lay.xs_bytes); };
-  auto sbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.ss_off + (i & 1) * lay.buf_bytes); };
-  auto hbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.sh_off + (i & 1) * lay.buf_bytes); };
-  auto stbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.st_off + (i & 1) * lay.st_bytes); };
+  auto sbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.ss_off + (i % d.nsb) * lay.buf_bytes); };
+  auto hbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.sh_off + (i % d.nsb) * lay.buf_bytes); };
+  auto stbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.st_off + (i % 3) * lay.st_bytes); };
 
   const int tid = threadIdx.x;
   const bool mma_group = tid < kGroup;
@@ -332,19 +340,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   for (int k = item_begin; k < item_end; ++k) {
     const int s = k / d.NCH;
     ntile += slice_tile(d, s + 1) - slice_tile(d, s);
-  }
+  }  // once per CTA
   if (ntile == 0) return;
 
   // ---- one-time setup (all 512 threads) ----
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + lay.mbar_off);
-  unsigned long long* empty = full + 3;
+  unsigned long long* empty = full + 4;
+  unsigned long long* sready = empty + 4;  // [2] S(i) written by all 8 MMA warps
+  unsigned long long* wready = sready + 2; // [2] w(i), fac(i) written by all 8 update warps
+  unsigned long long* sfree = wready + 2;  // [nsb] every MMA warp is done with w(i) (P3(i))
   if (tid == 0) {
     for (int b = 0; b < nbuf; ++b) {
       mbar_init(full + b, 1);   // the producer's arrive.expect_tx; TMA completes the bytes
       mbar_init(empty + b, 8);  // one arrive per MMA warp after its last read of the tile
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(sready + b, 8);
+      mbar_init(wready + b, 8);
+    }
+    for (int b = 0; b < d.nsb; ++b) mbar_init(sfree + b, 8);
     mbar_fence_init();
   }
+  // Cross-group hand-offs on mbarriers: every warp arrives or waits on its own, so
+  // no warp of one group ever waits for a slower warp of the same group.
+  auto warp_arrive = [&](unsigned long long* bar) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+  };
+  auto s_arrive = [&](int i) { warp_arrive(sready + (i & 1)); };
+  auto s_wait = [&](int i) { mbar_wait(sready + (i & 1), (i >> 1) & 1); };
+  auto w_arrive = [&](int i) { warp_arrive(wready + (i & 1)); };
+  auto w_wait = [&](int i) { mbar_wait(wready + (i & 1), (i >> 1) & 1); };
   if (tid < d.QCpad) facb[tid] = facb[d.QCpad + tid] = 1.0;
   load_exp_table(etab, tid);
   __syncthreads();
@@ -371,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     // Producer (MMA thread 0): X(f) into slot f % nbuf once the slot's previous
     // tile has been released by all 8 MMA warps (empty barrier).
     auto load_next_x = [&](int f) {
-      if (gtid == 0) {
+      if (gtid == 0 && !(pa.dbg & 4)) {
         const int b = f % nbuf, u = f / nbuf;
         if (u > 0) mbar_wait(empty + b, (u - 1) & 1);
         mbar_expect_tx(full + b, tile_tx);
@@ -383,15 +409,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       }
       cursor_next(xc, d);
     };
-    auto x_wait = [&](int i) { mbar_wait(full + i % nbuf, (i / nbuf) & 1); };
+    auto x_wait = [&](int i) {
+      if (!(pa.dbg & 4)) mbar_wait(full + i % nbuf, (i / nbuf) & 1);
+    };
     auto x_release = [&](int i) {
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + i % nbuf);
+      if (lane == 0 && !(pa.dbg & 4)) mbar_arrive(empty + i % nbuf);
     };
     // P1: S[c][j] = Σ_l W[l][c]·X[l][j]; warp = 8 pixels × one band half.
     auto phase1 = [&](int i) {
-      if (MODE == kModeInit || (pa.dbg & 1)) return;
-      const int chunk = p1c.item % d.NCH;
+      if (i >= d.nsb) mbar_wait(sfree + i % d.nsb, ((i / d.nsb) - 1) & 1);  // w(i−nsb) consumed
+      if (MODE == kModeInit || (pa.dbg & 65)) return;
+      const int chunk = p1c.chunk;
       if (chunk != wchunk) {  // restage W once every MMA warp is past its previous P1
         bar_sync(bars::kMma, kGroup);
         for (int e = gtid; e < d.Lpad * d.QCpad; e += kGroup) {
@@ -406,21 +435,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       double c1[kMaxCT][2];
 #pragma unroll
       for (int c = 0; c < kMaxCT; ++c) c1[c][0] = c1[c][1] = 0.0;
-      const double* wcol = ws + t4 * WST + g;
-      // X[l][pt·8+g], l = kk·4 + t4: (l & 7) depends only on the parity of kk
-      const int xo0 = xoff<XT>(t4, pt * 8 + g, xrows), xo1 = xoff<XT>(4 + t4, pt * 8 + g, xrows);
-      // band halves of even length: K4 = Lpad/4 k-steps is even, split at h0 = 2⌊K4/4⌋
+      // Bands are taken in pairs of k-steps covering 8 bands: within pair m, lane
+      // (g, t4) feeds band 8m + 2·t4 + par (par = 0, 1).  This band order makes
+      // both the X B-fragment (rows 2·t4+par hit distinct 128-byte swizzle chunks)
+      // and the W A-fragment (row stride 2·WST words ≡ 8 mod 32) conflict-free.
+      const double* wcol = ws + 2 * t4 * WST + g;
+      const int xo0 = xoff<XT>(2 * t4, pt * 8 + g, xrows), xo1 = xoff<XT>(2 * t4 + 1, pt * 8 + g, xrows);
+      // band halves of even k-step length: K4 = Lpad/4 is even, split at h0 = 2⌊K4/4⌋
       const int h0 = 2 * (d.Lpad / 16);
-      const int kb = half ? h0 : 0;
-      const int kn = half ? d.Lpad / 4 - h0 : h0;
+      const int mb = (half ? h0 : 0) / 2;
+      const int mn = (half ? d.Lpad / 4 - h0 : h0) / 2;
 #pragma unroll 2
-      for (int k2 = 0; k2 < kn / 2; ++k2) {
-        const int kk = kb + 2 * k2;
-        const XT* xr = xs + (kk >> 1) * 8 * kXRow<XT>;
+      for (int m2 = 0; m2 < mn; ++m2) {
+        const int m = mb + m2;
+        const XT* xr = xs + m * 8 * kXRow<XT>;
         const double bx0 = static_cast<double>(xr[xo0]);
         const double bx1 = static_cast<double>(xr[xo1]);
-        const double* w0 = wcol + kk * 4 * WST;
-        const double* w1 = w0 + 4 * WST;
+        const double* w0 = wcol + m * 8 * WST;
+        const double* w1 = w0 + WST;
 #pragma unroll
         for (int ct = 0; ct < kMaxCT; ++ct) dmma(c1[ct], w0[ct * 8], bx0);
 #pragma unroll
@@ -433,13 +465,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
             make_double2(c1[ct][0], c1[ct][1]);
     };
 
-    load_next_x(0);
-    if (ntile > 1) load_next_x(1);
+    for (int f = 0; f < nbuf - 1 && f < ntile; ++f) load_next_x(f);  // X(0 .. nbuf−2) in flight
     x_wait(0);
     phase1(0);
     cursor_next(p1c, d);
-    bar_arrive(bars::kS + 0, kThreads);
+    s_arrive(0);
     for (int it = 0; it < ntile; ++it) {
+      // X(i+nbuf−1) into X(i−1)'s slot (released after P3(i−1)): nbuf−1 tiles of lead
+      if (it + nbuf - 1 < ntile) load_next_x(it + nbuf - 1);
       if (it + 1 < ntile) {
         {
           EDAA_TSTART();
@@ -451,14 +484,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           phase1(it + 1);
           EDAA_TSTOP(1);
         }
-        // three slots: X(i+2) reuses X(i−1)'s slot, released after P3(i−1)
-        if (nbuf > 2 && it + 2 < ntile) load_next_x(it + 2);
         cursor_next(p1c, d);
-        bar_arrive(bars::kS + ((it + 1) & 1), kThreads);
+        s_arrive(it + 1);
       }
       {
         EDAA_TSTART();
-        bar_sync(bars::kW + (it & 1), kThreads);  // w(i), fac(i) ready
+        w_wait(it);  // w(i), fac(i) ready
         EDAA_TSTOP(2);
       }
       if (MODE != kModeObj) {
@@ -480,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         const XT* xs = xbuf(it);
         const double* w = sbuf(it);
         EDAA_TSTART();
-        if (!(pa.dbg & 1)) {
+        if (!(pa.dbg & 129)) {
           switch (my_x + (my_pseudo ? 8 : 0)) {  // warp-uniform: the DMMAs below are unpredicated
             case 1: accumulate_tiles<1, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
             case 2: accumulate_tiles<2, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
@@ -499,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         }
         EDAA_TSTOP(3);
         if (p3c.tile + 1 == p3c.tend) {  // the item's last tile: flush and restart its partials
-          const int slice = p3c.item / d.NCH, col0 = (p3c.item % d.NCH) * d.QCpad;
+          const int slice = p3c.slice, col0 = p3c.chunk * d.QCpad;
 #pragma unroll
           for (int i = 0; i < RTW; ++i) {
             const int rt = gwarp + 8 * i;
@@ -518,8 +549,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         }
       }
       x_release(it);  // this warp is done with X(i) (P1(i) and P3(i))
+      warp_arrive(sfree + it % d.nsb);  // … and with S(i)/w(i)
       cursor_next(p3c, d);
-      if (nbuf == 2 && it + 2 < ntile) load_next_x(it + 2);  // two slots: reuse X(i)'s
     }
   } else {
     // ========================== update group ==========================
@@ -527,29 +558,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     cursor_set(sc, d, item_begin);
     cursor_set(p2c, d, item_begin);
     int cchunk = -1;
-    {
-      const ChunkInfo ci = chunk_info(d, sc.item);
-      issue_state<MODE>(pa, stbuf(0), sc.tile * kNP, ci.srow0, ci.ncol, gtid);
-      cursor_next(sc, d);
+    auto next_state = [&](int f) {  // one commit group per call (empty past the end)
+      if (f < ntile) {
+        const ChunkInfo cn = chunk_info(d, sc.chunk);
+        issue_state<MODE>(pa, stbuf(f), sc.tile * kNP, cn.srow0, cn.ncol, gtid);
+        cursor_next(sc, d);
+      } else {
+        cp_async_commit();
+      }
+    };
+    next_state(0);
+    next_state(1);
+    if (pa.dbg & 256) {  // development: bare hand-shake, no update work
+      for (int it = 0; it < ntile; ++it) {
+        s_wait(it);
+        w_arrive(it);
+      }
+      return;
     }
     for (int it = 0; it < ntile; ++it) {
-      const ChunkInfo ci = chunk_info(d, p2c.item);
+      const ChunkInfo ci = chunk_info(d, p2c.chunk);
       const int j0 = p2c.tile * kNP;
-      const bool item_first = p2c.tile == slice_tile(d, p2c.item / d.NCH);
+      const bool item_first = p2c.tile == slice_tile(d, p2c.slice);
       const bool item_last = p2c.tile + 1 == p2c.tend;
       bar_sync(bars::kUpd, kGroup);  // everyone is done with st(i−1) and the previous item's scalars
-      const bool more = it + 1 < ntile;
-      if (more) {
-        const ChunkInfo cn = chunk_info(d, sc.item);
-        issue_state<MODE>(pa, stbuf(it + 1), sc.tile * kNP, cn.srow0, cn.ncol, gtid);
-        cursor_next(sc, d);
-      }
+      next_state(it + 2);            // into st(i−1)'s slot
       if (ci.chunk != cchunk) {  // per-column constants and G blocks of the new chunk
         if (gtid < d.QCpad) {
           const int c = gtid;
           const bool real = c < ci.ncol;
-          c_m[c] = (MODE == kModeB && real) ? pa.colm[ci.col0 + c] : 0.0;
-          c_logS[c] = (MODE == kModeB && real) ? pa.collogS[ci.col0 + c] : 0.0;
+          // log b_old = ℓ − (m + log S): one subtraction per element
+          c_m[c] = (MODE == kModeB && real) ? pa.colm[ci.col0 + c] + pa.collogS[ci.col0 + c] : 0.0;
           c_eta[c] = (MODE == kModeB && real) ? pa.eta_b[ci.run0 + c / p] : 0.0;
         }
         if (MODE == kModeA || MODE == kModeObj) {
@@ -568,11 +607,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         }
         if (gtid < d.RC) obj_run[gtid] = 0.0;
       }
-      if (more) cp_async_wait1(); else cp_async_wait0();
+      cp_async_wait2();  // st(i) landed (st(i+1), st(i+2) may still fly)
       bar_sync(bars::kUpd, kGroup);  // st(i), constants and resets visible
       {
         EDAA_TSTART();
-        bar_sync(bars::kS + (it & 1), kThreads);  // S(i) ready
+        s_wait(it);  // S(i) ready
         EDAA_TSTOP(4);
       }
       EDAA_TSTART();
@@ -623,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
                 v = 0.1 * splitmix_unit_at(pa.seeds[r], static_cast<uint64_t>(i) * d.N +
                                                             static_cast<uint64_t>(pix));
               } else {
-                double lb = st[c * kNP + j] - c_m[c] - c_logS[c];         // log b_old
+                double lb = st[c * kNP + j] - c_m[c];                      // log b_old
                 lb = (lb < log_floor()) ? log_floor() : lb;                // log max(b, 1e-30)
                 v = lb + (ss[c * kSST + j] + sh[c * kSST + j]) * c_eta[c]; // + η_b·(−∇_B)
               }
@@ -659,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       EDAA_TSTOP(5);
       if (item_last) {  // the item's softmax / objective partials
         bar_sync(bars::kUpd, kGroup);
-        const int slice = p2c.item / d.NCH;
+        const int slice = p2c.slice;
         if (MODE == kModeB || MODE == kModeInit) {
           if (gtid < d.QCpad) {
             pa.part_m[static_cast<size_t>(slice) * d.Qs + ci.col0 + gtid] = m_run[gtid];
@@ -669,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           if (gtid < ci.RCe) pa.part_obj[static_cast<size_t>(slice) * d.M + ci.run0 + gtid] = obj_run[gtid];
         }
       }
-      bar_arrive(bars::kW + (it & 1), kThreads);  // w(i), fac(i) ready for P3(i)
+      w_arrive(it);  // w(i), fac(i) ready for P3(i)
       cursor_next(p2c, d);
     }
   }

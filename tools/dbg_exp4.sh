@@ -1,0 +1,1 @@
+for dbg in 450 454 $((450+16)) $((454+16)); do echo "EDAA_DBG=$dbg"; EDAA_DBG=$dbg python tools/pass_times.py ${1:-cfg2} 3 2>&1 | tail -1; done
