@@ -24,6 +24,12 @@
 
 using edaa::Dims;
 
+struct GraphKey {
+  Dims d;
+  size_t T, K2;
+  uint64_t gen;
+};
+
 struct edaa_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -57,6 +63,13 @@ struct edaa_ctx {
   int dbg = 0;                // EDAA_DBG: development switches, results invalid when set
   int num_sms = 148;
   alignas(64) CUtensorMap xmap;  // TMA descriptor of X for the current solve
+  // CUDA graph of the last solve's device schedule and what it was captured for
+  bool no_graph = false;
+  uint64_t gen = 0;  // bumped whenever a device buffer or the image moves
+  uint64_t image_gen = 0;
+  cudaGraphExec_t graph_exec = nullptr;
+  GraphKey graph_key{};
+  uint64_t graph_launches = 0;
   // host copies of the per-run records
   std::vector<double> h_fit, h_mu, h_eta_a, h_eta_b, h_fail_value, h_trace;
   std::vector<int> h_fail_code;
@@ -80,8 +93,11 @@ int cuda_fail(edaa_ctx* c, cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #call); \
   } while (0)
 
+uint64_t g_realloc_count = 0;  // any device (re)allocation invalidates captured graphs
+
 cudaError_t ensure(edaa_ctx::Buf& b, size_t bytes) {
   if (b.cap >= bytes && b.p) return cudaSuccess;
+  ++g_realloc_count;
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.cap = 0;
@@ -390,6 +406,11 @@ bool all_finite(const double* v, size_t n) {
   return true;
 }
 
+int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook);
+
+// One solve: per-run seeds and step factors go up, then the whole device
+// schedule (≈ 3 + T·(3 + 4·K2) + 7 kernels) runs — replayed from a CUDA graph
+// captured on the first solve of a given shape (EDAA_NO_GRAPH=1 disables).
 int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   Dims d{};
   int rc = make_dims(c, prm, &d);
@@ -401,9 +422,46 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   if (rc) return rc;
   rc = make_xmap(c, d);
   if (rc) return rc;
+  c->gen = g_realloc_count * 1000003ull + c->image_gen;
   cudaStream_t st = c->stream;
   EDAA_CUDA(c, cudaMemcpyAsync(c->seeds.p, prm->seeds, d.M * 8, cudaMemcpyHostToDevice, st));
   EDAA_CUDA(c, cudaMemcpyAsync(c->gamma.p, prm->gammas, d.M * 8, cudaMemcpyHostToDevice, st));
+  const bool use_graph = !hook && !c->profile && !c->no_graph;
+  if (!use_graph) return enqueue_solve(c, prm, hook);
+  GraphKey key{};
+  key.d = d;
+  key.T = c->T;
+  key.K2 = prm->inner_iters_b;
+  key.gen = c->gen;
+  if (!(c->graph_exec && std::memcmp(&key, &c->graph_key, sizeof key) == 0)) {
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    c->graph_exec = nullptr;
+    const uint64_t l0 = c->launches;
+    EDAA_CUDA(c, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_solve(c, prm, nullptr);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ce != cudaSuccess) return cuda_fail(c, ce, "cudaStreamEndCapture");
+    const cudaError_t ie = cudaGraphInstantiate(&c->graph_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return cuda_fail(c, ie, "cudaGraphInstantiate");
+    c->graph_launches = c->launches - l0;
+    c->launches = l0;
+    c->graph_key = key;
+  }
+  EDAA_CUDA(c, cudaGraphLaunch(c->graph_exec, st));
+  c->launches += c->graph_launches;
+  return EDAA_OK;
+}
+
+int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
+  const Dims d = c->d;
+  int rc = EDAA_OK;
+  cudaStream_t st = c->stream;
   EDAA_CUDA(c, cudaMemsetAsync(c->fail_key.p, 0xFF, d.M * 8, st));
   EDAA_CUDA(c, cudaMemsetAsync(c->fail_code.p, 0, d.M * 4, st));
   EDAA_CUDA(c, cudaMemsetAsync(c->fail_value.p, 0, d.M * 8, st));
@@ -519,6 +577,7 @@ int edaa_create(int device, edaa_ctx** out) {
     return EDAA_ERR_CUDA;
   }
   if (const char* dbg = std::getenv("EDAA_DBG")) c->dbg = std::atoi(dbg);
+  if (const char* ng = std::getenv("EDAA_NO_GRAPH")) c->no_graph = ng[0] == '1';
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* kp = std::getenv("EDAA_KPROF"))
     if (kp[0] == '1' && cudaMalloc(&c->kprof_buf, 24 * 8) == cudaSuccess) cudaMemset(c->kprof_buf, 0, 24 * 8);
@@ -541,6 +600,7 @@ int edaa_destroy(edaa_ctx* c) {
     if (b->p) cudaFree(b->p);
   if (c->X) cudaFree(c->X);
   if (c->xnorm) cudaFree(c->xnorm);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   cudaStreamDestroy(c->stream);
   delete c;
   return EDAA_OK;
@@ -559,6 +619,7 @@ static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels, int xbytes) {
   c->N = static_cast<int>(pixels);
   c->Npad = (c->N + edaa::kNP - 1) / edaa::kNP * edaa::kNP;
   c->xbytes = xbytes;
+  ++c->image_gen;  // X contents change: tensor map and graph are rebuilt
   const size_t xb = static_cast<size_t>(c->L) * c->Npad * xbytes;
   if (c->x_cap < xb) {
     if (c->X) cudaFree(c->X);
