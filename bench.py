@@ -271,6 +271,25 @@ def main():
 
     # ---- e2e through the public API (pinned host X; H2D + solve + select + D2H) ----
     e2e = None
+    if not args.no_e2e and world > 1:
+        # public multi-GPU API: pinned host X per rank, sharded solve, record
+        # all-gather, selection, broadcast of the selected run's factors
+        import torch.distributed as dist
+        from paper_2209_11002_b200 import distributed
+        x_pin = torch.from_numpy(x).pin_memory().numpy()
+        ecfg = edaa.EnsembleConfig(runs=M * world, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
+        distributed.run_ensemble_sharded(x_pin, ecfg, device=local)  # warm
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            distributed.run_ensemble_sharded(x_pin, ecfg, device=local)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=x_dev.device)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": M * world * T * args.steps / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(x.nbytes + 16 * M),
+               "d2h_bytes_per_step": int(8 * (2 * p * N + L * p + (T + 1)) + 32 * M)}
+        dev.set_image(x_dev)
     if not args.no_e2e and world == 1:
         x_pin = torch.from_numpy(x).pin_memory().numpy()
         ecfg = edaa.EnsembleConfig(runs=M, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))

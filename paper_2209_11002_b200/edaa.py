@@ -318,6 +318,23 @@ class Device:
         self._check(rc)
         return [int(i) for i in np.flatnonzero(cand)], int(sel.value), fmin.value
 
+    # -- primitives on the resident image ------------------------------------------
+    def fit_l1(self, E, A) -> float:
+        E = np.ascontiguousarray(E, dtype=np.float64)
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        out = C.c_double()
+        self._check(self.lib.edaa_fit_l1(self.h, E.ctypes.data_as(C.c_void_p),
+                                         A.ctypes.data_as(C.c_void_p), E.shape[1], C.byref(out)))
+        return out.value
+
+    def estimate_abundances(self, E, iters: int, eta: float) -> np.ndarray:
+        E = np.ascontiguousarray(E, dtype=np.float64)
+        A = np.zeros((E.shape[1], self.N))
+        self._check(self.lib.edaa_estimate_abundances(self.h, E.ctypes.data_as(C.c_void_p), E.shape[1],
+                                                      int(iters), float(eta),
+                                                      A.ctypes.data_as(C.c_void_p)))
+        return A
+
 
 def _result(dev: Device, run_idx: int, seed: int, gamma: float, traces) -> RunResult:
     A, B, E = dev.factors(run_idx)
@@ -378,3 +395,59 @@ def run_ensemble(x, config: EnsembleConfig, device: int = 0):
     cand, sel, fmin = dev.select(config.fit_slack)
     report = SelectionReport(recs, cand, sel, fmin)
     return _result(dev, sel, seeds[sel], gammas[sel], dev.traces()), report
+
+
+def fit_l1(x, E, A, device: int = 0) -> float:
+    """Σ|X − E·A| (ensemble.cpp:29-39) on the GPU."""
+    E = np.asarray(E, dtype=np.float64)
+    A = np.asarray(A, dtype=np.float64)
+    xf = validate_image(x)
+    if E.shape[0] != xf.shape[0] or A.shape != (E.shape[1], xf.shape[1]):
+        raise EdaaError("fit_l1: shape mismatch")
+    dev = Device.get(device)
+    dev.set_image(xf)
+    return dev.fit_l1(E, A)
+
+
+def _column_norm(E, j) -> float:
+    s = 0.0  # sequential, as Matrix::column_norm (matrix.cpp:44-51); builtin sum() compensates
+    for v in E[:, j]:
+        s += float(v) * float(v)
+    return float(np.sqrt(s))
+
+
+def coherence(E, normalized: bool = False) -> float:
+    """Largest off-diagonal endmember inner product (ensemble.cpp:41-60); a p×p
+    host reduction, like the reference's."""
+    E = np.asarray(E, dtype=np.float64)
+    p = E.shape[1]
+    best = -np.inf
+    for i in range(p):
+        for j in range(i + 1, p):
+            dot = 0.0
+            for r in range(E.shape[0]):
+                dot += E[r, i] * E[r, j]
+            if normalized:
+                ni, nj = _column_norm(E, i), _column_norm(E, j)
+                if ni == 0.0 or nj == 0.0:
+                    continue
+                dot /= ni * nj
+            best = max(best, dot)
+    return 0.0 if best == -np.inf else float(best)
+
+
+def estimate_abundances(x, E, iters: int, eta: float, device: int = 0) -> np.ndarray:
+    """A for fixed endmembers E, `iters` entropic steps from 1/p (solver.cpp:240-259)."""
+    E = np.asarray(E, dtype=np.float64)
+    xf = validate_image(x)
+    if not np.all(np.isfinite(E)):
+        raise EdaaError("estimate_abundances: non-finite input")
+    if E.shape[0] != xf.shape[0]:
+        raise EdaaError("estimate_abundances: band count mismatch")
+    if E.ndim != 2 or E.shape[1] < 1:
+        raise EdaaError("estimate_abundances: need at least one endmember")
+    if not (eta > 0.0) or not np.isfinite(eta):
+        raise EdaaError("estimate_abundances: eta must be positive")
+    dev = Device.get(device)
+    dev.set_image(xf)
+    return dev.estimate_abundances(E, iters, eta)

@@ -45,3 +45,27 @@ def test_restated_reference_unit_tests_pass_on_gpu():
     print(r.stderr)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "A/B" in r.stdout
+
+
+ACC = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(ACC), reason="oracle/_ref/acceptance_b200 not built "
+                    "(make -C oracle acceptance, needs the reference sources)")
+def test_reference_acceptance_gate_links_against_dropin():
+    out = subprocess.run(["ldd", ACC], capture_output=True, text=True).stdout
+    assert "libarchetype_b200.so" in out and "not found" not in out
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(ACC), reason="oracle/_ref/acceptance_b200 not built")
+def test_reference_acceptance_gate_passes_on_gpu():
+    """The reference's own release gate (proj/tests/acceptance.cpp, built in place
+    against include/archetype and libarchetype_b200.so) — every check except the
+    absent-dataset Samson check (acceptance.cpp:323-346) must pass on the GPU."""
+    r = subprocess.run([ACC], capture_output=True, text=True, cwd=ROOT, timeout=900)
+    print(r.stdout)
+    print(r.stderr)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "all checks passed" in r.stdout
+    assert r.stdout.count("PASS") >= 8

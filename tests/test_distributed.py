@@ -1,0 +1,76 @@
+"""Ensemble sharding across ranks (paper_2209_11002_b200/distributed.py), world_size 2
+on CPU with gloo.  The per-rank solve is the CPU oracle here (test infrastructure
+standing in for the GPU solve); what is under test is the sharding, the record
+all-gather, the selection on every rank and the broadcast of the selected run."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2209_11002_b200 import distributed, edaa, synth
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def oracle_local_solver(x, config, first, count):
+    from oracle import Oracle
+    orc = Oracle()
+    seeds, gammas = edaa.ensemble_plan(config, first=first, count=count)
+    recs, results = [], {}
+    s = config.solver
+    for k in range(count):
+        m = first + k
+        r = orc.run(np.asarray(x, dtype=np.float64), s.endmembers, T=s.outer_iters,
+                    K1=s.inner_iters_a, K2=s.inner_iters_b, gamma=gammas[k], seed=seeds[k])
+        recs.append(edaa.RunRecord(m, seeds[k], gammas[k], r.fit_l1, r.coherence, 0.0, True, ""))
+        results[m] = edaa.RunResult(r.E, r.A, r.B, r.fit_l1, r.coherence, seeds[k], gammas[k], r.trace)
+    return distributed.LocalBatch(first, recs, lambda m: results[m])
+
+
+def _worker(rank, world, port, runs, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x = synth.small_scene(16, 200, 3, seed=4)
+    cfg = edaa.EnsembleConfig(runs=runs, solver=edaa.SolverConfig(endmembers=3, outer_iters=6))
+    res, rep = distributed.run_ensemble_sharded(x, cfg, local_solver=oracle_local_solver)
+    np.savez(out % rank, selected=rep.selected, cand=np.array(rep.candidate_set),
+             fits=np.array([r.fit_l1 for r in rep.per_run]), A=res.abundances, B=res.contributions,
+             E=res.endmembers, trace=res.objective_trace)
+    dist.destroy_process_group()
+
+
+def test_shard_bounds_cover_every_run_once():
+    for runs in (1, 2, 5, 50, 64):
+        for world in (1, 2, 3, 8):
+            seen = []
+            for r in range(world):
+                f, c = distributed.shard_bounds(runs, world, r)
+                seen += list(range(f, f + c))
+            assert seen == list(range(runs))
+
+
+@pytest.mark.skipif(not __import__("oracle").available_kinds(), reason="oracle not built")
+@pytest.mark.parametrize("runs", [7, 1])
+def test_sharded_selection_matches_single_process(tmp_path, runs):
+    import torch.multiprocessing as mp
+    from oracle import Oracle
+    out = str(tmp_path / "rank%d.npz")
+    mp.spawn(_worker, args=(2, free_port(), runs, out), nprocs=2, join=True)
+    r0, r1 = np.load(out % 0), np.load(out % 1)
+    x = synth.small_scene(16, 200, 3, seed=4).astype(np.float64)
+    ref = Oracle().run_ensemble(x, 3, M=runs, T=6)
+    for r in (r0, r1):  # every rank holds the same answer
+        assert int(r["selected"]) == ref.selected
+        assert list(r["cand"]) == ref.candidates
+        assert np.array_equal(r["fits"], ref.fits)
+        assert np.array_equal(r["A"], ref.A) and np.array_equal(r["B"], ref.B)
+        assert np.array_equal(r["trace"], ref.trace)

@@ -220,3 +220,31 @@ def test_fp64_image_path(oracle_kinds):
     if oracle_kinds:
         ref2 = Oracle(oracle_kinds[0]).run(x2, 6, T=30, gamma=8.0, seed=3)
         check_run(r2.objective_trace, r2.abundances, r2.contributions, ref2.trace, ref2.A, ref2.B)
+
+
+def test_python_primitives_match_reference(oracle_kinds):
+    """fit_l1 (ensemble.cpp:29-39) and estimate_abundances (solver.cpp:240-259)
+    through the package API (device kernels) against the oracle / a fp64
+    restatement of the reference loop."""
+    from oracle import Oracle
+    rng = np.random.default_rng(11)
+    L, N, p = 24, 700, 4
+    E = rng.random((L, p))
+    A = rng.dirichlet(np.ones(p), N).T
+    x = (E @ A + 0.01 * rng.random((L, N))).astype(np.float32)
+    orc = Oracle(oracle_kinds[0])
+    ref = orc.fit_l1(x.astype(np.float64), E, A)
+    assert abs(edaa.fit_l1(x, E, A) - ref) <= 1e-12 * ref
+    # estimate_abundances: restated loop (matmul order does not matter at 1e-12)
+    X = x.astype(np.float64)
+    a = np.full((p, N), 1.0 / p)
+    eta = 0.5
+    for _ in range(7):
+        g = eta * (E.T @ (X - E @ a))
+        z = np.log(np.maximum(a, 1e-30)) + g
+        z = np.exp(z - z.max(axis=0))
+        a = z / z.sum(axis=0)
+    got = edaa.estimate_abundances(x, E, 7, eta)
+    assert np.abs(got - a).max() <= 1e-12
+    with pytest.raises(edaa.EdaaError, match="eta must be positive"):
+        edaa.estimate_abundances(x, E, 7, 0.0)

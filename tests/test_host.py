@@ -149,3 +149,17 @@ def test_abundance_cap():
     _, _, a = synth.generate(spec, pixels=5000)
     assert a.max() <= 0.8 + 1e-12
     np.testing.assert_allclose(a.sum(axis=0), 1.0, atol=1e-12)
+
+
+def test_coherence_matches_oracle(oracle_kinds):  # ensemble.cpp:41-60, test_ensemble.cpp:91-116
+    e = np.array([[1.0, 0.0], [0.0, 1.0], [0.8, 0.8]])
+    assert edaa.coherence(np.array([[1.0], [2.0]])) == 0.0
+    if not oracle_kinds:
+        pytest.skip("oracle not built")
+    from oracle import Oracle
+    orc = Oracle(oracle_kinds[0])
+    rng = np.random.default_rng(3)
+    for _ in range(10):
+        e = rng.random((int(rng.integers(1, 40)), int(rng.integers(2, 9))))
+        for norm in (False, True):
+            assert edaa.coherence(e, norm) == orc.coherence(e, norm)
