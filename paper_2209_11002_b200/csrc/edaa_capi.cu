@@ -202,13 +202,12 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.Lrows = d.Lpad + d.QCpad;
   d.K1 = static_cast<int>(prm->inner_iters_a);
   d.ncta = c->num_sms;
-  // Ring depths, as deep as shared memory allows: X tiles (≥ 2) and projection /
-  // weight tiles (≥ 2); the X ring is shortened first.
-  d.nbuf = 4;
-  d.nsb = 2;  // P1(i) reuses w(i−2)'s buffer after the sfree barrier
-  while (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem) && (d.nbuf > 2 || d.nsb > 2)) {
-    if (d.nbuf > 3 || (d.nbuf > 2 && d.nsb == 2)) --d.nbuf;
-    else --d.nsb;
+  // X ring depth and W chunk buffers, the deepest that fits shared memory.
+  static const int kRing[][2] = {{4, 2}, {3, 2}, {3, 1}, {2, 2}, {2, 1}};
+  for (const auto& rw : kRing) {
+    d.nbuf = rw[0];
+    d.nwb = rw[1];
+    if (edaa::pass_smem_bytes(d, d.nbuf) <= static_cast<size_t>(edaa::kMaxSmem)) break;
   }
   if (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem))
     return set_err(c, EDAA_ERR_UNSUPPORTED, "tile working set exceeds shared memory");

@@ -48,9 +48,10 @@ __device__ __forceinline__ double max_like_std(double top, double s) {
 //   st  2 × state tile         [QCpad][kNP] fp64 (A or logits of the chunk's columns)
 //   gs  G blocks of the chunk's runs, then per-column and per-run scalars.
 struct SmemLayout {
-  int xs_off, xs_bytes, ws_off, ss_off, sh_off, st_off, buf_bytes, st_bytes, gs_off, col_off, tab_off,
-      mbar_off, total;
+  int xs_off, xs_bytes, ws_off, ws_bytes, ss_off, sh_off, st_off, buf_bytes, st_bytes, gs_off, col_off,
+      tab_off, slt_off, mbar_off, total;
 };
+constexpr int kNSB = 2;  // projection / weight tile buffers: P1(i) reuses w(i−2)'s after sfree
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 
@@ -92,13 +93,14 @@ __host__ __device__ inline SmemLayout smem_layout(const Dims& d, int nbuf) {
   s.xs_off = off;  // TMA destination: 1024-byte aligned, 128-byte swizzled rows
   s.xs_bytes = x_tile_bytes(d);
   off += nbuf * s.xs_bytes;
-  s.ws_off = off;
-  off += align16(d.Lpad * w_stride(d.QCpad) * 8);
+  s.ws_off = off;  // 2 W chunks: the current one and the next item's, prefetched by cp.async
+  s.ws_bytes = align16(d.Lpad * w_stride(d.QCpad) * 8);
+  off += d.nwb * s.ws_bytes;
   s.buf_bytes = align16(d.QCpad * kSST * 8);
   s.ss_off = off;  // nsb buffers of projection half 0 / weights
-  off += d.nsb * s.buf_bytes;
+  off += kNSB * s.buf_bytes;
   s.sh_off = off;  // nsb buffers of projection half 1
-  off += d.nsb * s.buf_bytes;
+  off += kNSB * s.buf_bytes;
   s.st_bytes = align16(d.QCpad * kNP * 8);
   s.st_off = off;
   off += 3 * s.st_bytes;  // state tiles i, i+1, i+2 in flight
@@ -109,6 +111,8 @@ __host__ __device__ inline SmemLayout smem_layout(const Dims& d, int nbuf) {
   off += align16((7 * d.QCpad + 5 * d.RC) * 8);
   s.tab_off = off;  // 2^(i/64) table of exp_nonpos
   off += 64 * 8;
+  s.slt_off = off;  // first tile of every pixel slice (nslices + 1 ints)
+  off += align16((d.nslices + 1) * 4);
   s.mbar_off = off;  // full[4], empty[4] X ring; sready[2], wready[2] hand-offs; sfree[4]
   off += 16 * 8;
   s.total = off;

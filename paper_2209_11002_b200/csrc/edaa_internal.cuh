@@ -53,9 +53,9 @@ struct Dims {
   int Lrows;  // Lpad + QCpad (A-pass pseudo rows carry AAᵀ)
   int K1;
   int nbuf;   // X tile buffers in shared memory (2 = prefetch next tile)
+  int nwb;    // W chunk buffers: 2 = next chunk prefetched, 1 = restaged in place
   int xbytes; // 4: fp32 image, 8: fp64 image (inputs not exactly representable in fp32)
   int ncta;   // persistent pass CTAs (one per SM)
-  int nsb;    // projection/weight tile buffers (2..4)
 };
 
 struct PassArgs {

@@ -263,29 +263,40 @@ __device__ __forceinline__ void issue_state(const PassArgs& pa, double* st, int 
 // the per-column constants when the chunk changes and flushing every item's
 // partials when its last tile retires.
 struct Cursor {
-  int item, slice, chunk, tile, tend;
+  int item, slice, chunk, tile, tstart, tend;
 };
 
-__device__ __forceinline__ int slice_tile(const Dims& d, int s) {
+__host__ __device__ __forceinline__ int slice_tile(const Dims& d, int s) {
   return (s * d.ntiles) / d.nslices;  // < 2^31: ntiles ≤ 2^25, nslices ≤ 296
 }
-__device__ __forceinline__ void cursor_set(Cursor& c, const Dims& d, int item) {
+// slt: the CTA's shared-memory copy of slice_tile(d, 0 .. nslices) (no divisions per tile)
+__device__ __forceinline__ void cursor_set(Cursor& c, const Dims& d, const int* slt, int item) {
   c.item = item;
   c.slice = item / d.NCH;
   c.chunk = item - c.slice * d.NCH;
-  c.tile = slice_tile(d, c.slice);
-  c.tend = slice_tile(d, c.slice + 1);
+  c.tile = c.tstart = slt[c.slice];
+  c.tend = slt[c.slice + 1];
 }
-__device__ __forceinline__ void cursor_next(Cursor& c, const Dims& d) {
+__device__ __forceinline__ void cursor_next(Cursor& c, const Dims& d, const int* slt) {
   if (++c.tile != c.tend) return;
   ++c.item;  // slice-major: the next chunk of the same slice, then the next slice
   if (++c.chunk == d.NCH) {
     c.chunk = 0;
     ++c.slice;
   }
-  c.tile = slice_tile(d, c.slice);
-  c.tend = slice_tile(d, c.slice + 1);
+  c.tile = c.tstart = slt[c.slice];
+  c.tend = slt[c.slice + 1];
 }
+// Position in a ring of n slots walked one step at a time (slot = i % n, phase = (i / n) & 1).
+struct Ring {
+  int slot, phase;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+};
 
 struct ChunkInfo {
   int chunk, run0, RCe, ncol, col0, srow0;
@@ -296,7 +307,7 @@ __device__ __forceinline__ ChunkInfo chunk_info(const Dims& d, int chunk) {
   ci.run0 = ci.chunk * d.RC;
   ci.RCe = min(d.RC, d.M - ci.run0);
   ci.ncol = ci.RCe * d.p;
-  ci.col0 = ci.chunk * d.QCpad;
+  ci.col0 = ci.chunk * kQMax;
   ci.srow0 = ci.run0 * d.p;
   return ci;
 }
@@ -307,21 +318,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   const Dims& d = pa.d;
   const int nbuf = d.nbuf;
   const SmemLayout lay = smem_layout(d, nbuf);
-  double* ws = reinterpret_cast<double*>(smem + lay.ws_off);
+  double* ws0 = reinterpret_cast<double*>(smem + lay.ws_off);  // W chunk buffers 0, 1
+  int* slt = reinterpret_cast<int*>(smem + lay.slt_off);
   double* gs = reinterpret_cast<double*>(smem + lay.gs_off);
   double* m_run = reinterpret_cast<double*>(smem + lay.col_off);
-  double* S_run = m_run + d.QCpad;
-  double* c_m = S_run + d.QCpad;      // normaliser max of the previous logits (B pass)
-  double* c_logS = c_m + d.QCpad;     // its log-sum
-  double* c_eta = c_logS + d.QCpad;   // η_b of the column's run (B pass)
-  double* facb = c_eta + d.QCpad;     // [2][QCpad] running-max rescale of tile i%2
-  double* obj_run = facb + 2 * d.QCpad;
+  double* S_run = m_run + kQMax;
+  double* c_m = S_run + kQMax;      // normaliser max of the previous logits (B pass)
+  double* c_logS = c_m + kQMax;     // its log-sum
+  double* c_eta = c_logS + kQMax;   // η_b of the column's run (B pass)
+  double* facb = c_eta + kQMax;     // [2][QCpad] running-max rescale of tile i%2
+  double* obj_run = facb + 2 * kQMax;
   double* hobj = obj_run + d.RC;
   double* etab = reinterpret_cast<double*>(smem + lay.tab_off);
-  auto xbuf = [&](int i) { return reinterpret_cast<XT*>(smem + lay.xs_off + (i % nbuf) * lay.xs_bytes); };
-  auto sbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.ss_off + (i % d.nsb) * lay.buf_bytes); };
-  auto hbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.sh_off + (i % d.nsb) * lay.buf_bytes); };
-  auto stbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.st_off + (i % 3) * lay.st_bytes); };
+  auto xslot = [&](int b) { return reinterpret_cast<XT*>(smem + lay.xs_off + b * lay.xs_bytes); };
+  auto sbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.ss_off + (i & 1) * lay.buf_bytes); };
+  auto hbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.sh_off + (i & 1) * lay.buf_bytes); };
+  auto stslot = [&](int b) { return reinterpret_cast<double*>(smem + lay.st_off + b * lay.st_bytes); };
 
   const int tid = threadIdx.x;
   const bool mma_group = tid < kGroup;
@@ -330,8 +342,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   const int g = lane >> 2, t4 = lane & 3;
   const int p = d.p;
   const int nRTx = d.Lpad / 8;
-  const int nRT = (MODE == kModeA) ? nRTx + d.QCpad / 8 : nRTx;
-  const int WST = w_stride(d.QCpad);
+  const int nRT = (MODE == kModeA) ? nRTx + kQMax / 8 : nRTx;
+  const int WST = w_stride(kQMax);
 
   const int K = d.NCH * d.nslices;
   const int item_begin = static_cast<int>((static_cast<long long>(blockIdx.x) * K) / gridDim.x);
@@ -348,7 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   unsigned long long* empty = full + 4;
   unsigned long long* sready = empty + 4;  // [2] S(i) written by all 8 MMA warps
   unsigned long long* wready = sready + 2; // [2] w(i), fac(i) written by all 8 update warps
-  unsigned long long* sfree = wready + 2;  // [nsb] every MMA warp is done with w(i) (P3(i))
+  unsigned long long* sfree = wready + 2;  // [kNSB] every MMA warp is done with w(i) (P3(i))
+  for (int i = tid; i <= d.nslices; i += kThreads) slt[i] = slice_tile(d, i);
   if (tid == 0) {
     for (int b = 0; b < nbuf; ++b) {
       mbar_init(full + b, 1);   // the producer's arrive.expect_tx; TMA completes the bytes
@@ -358,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       mbar_init(sready + b, 8);
       mbar_init(wready + b, 8);
     }
-    for (int b = 0; b < d.nsb; ++b) mbar_init(sfree + b, 8);
+    for (int b = 0; b < kNSB; ++b) mbar_init(sfree + b, 8);
     mbar_fence_init();
   }
   // Cross-group hand-offs on mbarriers: every warp arrives or waits on its own, so
@@ -371,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   auto s_wait = [&](int i) { mbar_wait(sready + (i & 1), (i >> 1) & 1); };
   auto w_arrive = [&](int i) { warp_arrive(wready + (i & 1)); };
   auto w_wait = [&](int i) { mbar_wait(wready + (i & 1), (i >> 1) & 1); };
-  if (tid < d.QCpad) facb[tid] = facb[d.QCpad + tid] = 1.0;
+  if (tid < kQMax) facb[tid] = facb[kQMax + tid] = 1.0;
   load_exp_table(etab, tid);
   __syncthreads();
 
@@ -386,51 +399,81 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     const int my_x = (nRTx - gwarp + 7) / 8;  // of which X rows (the rest: one pseudo tile)
     const bool my_pseudo = my_rt > my_x;
     Cursor xc, p1c, p3c;
-    cursor_set(xc, d, item_begin);
-    cursor_set(p1c, d, item_begin);
-    cursor_set(p3c, d, item_begin);
-    int wchunk = -1;
+    cursor_set(xc, d, slt, item_begin);
+    cursor_set(p1c, d, slt, item_begin);
+    cursor_set(p3c, d, slt, item_begin);
+    // W chunk double buffer: ws(wcur) holds chunk wchunk; the next item's chunk is
+    // prefetched by cp.async into the other buffer while the current one is in use.
+    int wcur = 0, wchunk = -1;
+    auto ws_buf = [&](int b) { return reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ws0) + b * lay.ws_bytes); };
+    auto w_fetch = [&](int chunk, int b) {  // one cp.async group per thread (possibly empty)
+      double* dstw = ws_buf(b);
+      constexpr int kV = kQMax / 2;  // 16-byte pieces per band row
+      for (int e = gtid; e < d.Lpad * kV; e += kGroup) {
+        const int l = e / kV, c2 = e - l * kV;
+        cp_async16(dstw + l * WST + 2 * c2, pa.W + static_cast<size_t>(l) * d.Qs + chunk * kQMax + 2 * c2);
+      }
+      cp_async_commit();
+    };
+    auto item_chunk = [&](int item) { return item - (item / d.NCH) * d.NCH; };
 
     const int xrows = x_rows(d), brows = x_box_rows(d);
     const int nbox = xrows / brows, nhalf = sizeof(XT) / 4;  // row boxes × column halves
     const unsigned tile_tx = static_cast<unsigned>(nbox * nhalf * brows * 128);
     // Producer (MMA thread 0): X(f) into slot f % nbuf once the slot's previous
     // tile has been released by all 8 MMA warps (empty barrier).
+    Ring ldr{0, 0}, xwr{0, 0}, p3r{0, 0};  // X ring: producer, P1 consumer, P3 consumer
     auto load_next_x = [&](int f) {
       if (gtid == 0 && !(pa.dbg & 4)) {
-        const int b = f % nbuf, u = f / nbuf;
-        if (u > 0) mbar_wait(empty + b, (u - 1) & 1);
+        const int b = ldr.slot;
+        if (f >= nbuf) mbar_wait(empty + b, ldr.phase ^ 1);
         mbar_expect_tx(full + b, tile_tx);
-        XT* dst = xbuf(f);
+        XT* dst = xslot(b);
         for (int h = 0; h < nhalf; ++h)
           for (int bx = 0; bx < nbox; ++bx)
             tma_load_2d(dst + h * xrows * (32 / nhalf) + bx * brows * (32 / nhalf), &xmap,
                         xc.tile * kNP + h * 16, bx * brows, full + b);
       }
-      cursor_next(xc, d);
+      ldr.next(nbuf);
+      cursor_next(xc, d, slt);
     };
-    auto x_wait = [&](int i) {
-      if (!(pa.dbg & 4)) mbar_wait(full + i % nbuf, (i / nbuf) & 1);
+    auto x_wait = [&]() {  // the next tile for P1; returns its slot
+      const int b = xwr.slot;
+      if (!(pa.dbg & 4)) mbar_wait(full + b, xwr.phase);
+      xwr.next(nbuf);
+      return b;
     };
-    auto x_release = [&](int i) {
+    auto x_release = [&]() {  // P3's tile
       __syncwarp();
-      if (lane == 0 && !(pa.dbg & 4)) mbar_arrive(empty + i % nbuf);
+      if (lane == 0 && !(pa.dbg & 4)) mbar_arrive(empty + p3r.slot);
+      p3r.next(nbuf);
     };
     // P1: S[c][j] = Σ_l W[l][c]·X[l][j]; warp = 8 pixels × one band half.
-    auto phase1 = [&](int i) {
-      if (i >= d.nsb) mbar_wait(sfree + i % d.nsb, ((i / d.nsb) - 1) & 1);  // w(i−nsb) consumed
+    auto phase1 = [&](int i, int xb) {
+      if (i >= kNSB) mbar_wait(sfree + (i & 1), ((i >> 1) - 1) & 1);  // w(i−2) consumed
       if (MODE == kModeInit || (pa.dbg & 65)) return;
       const int chunk = p1c.chunk;
-      if (chunk != wchunk) {  // restage W once every MMA warp is past its previous P1
-        bar_sync(bars::kMma, kGroup);
-        for (int e = gtid; e < d.Lpad * d.QCpad; e += kGroup) {
-          const int l = e / d.QCpad, c = e % d.QCpad;
-          ws[l * WST + c] = pa.W[static_cast<size_t>(l) * d.Qs + chunk * d.QCpad + c];
+      if (chunk != wchunk) {
+        // Switch to the prefetched buffer once every MMA warp is past its previous
+        // P1 (so the old buffer is free), then prefetch the following item's chunk.
+        if (d.nwb == 2) {
+          if (wchunk >= 0) wcur ^= 1;
+          cp_async_wait0();
+          bar_sync(bars::kMma, kGroup);
+          if (p1c.item + 1 < item_end && item_chunk(p1c.item + 1) != chunk)
+            w_fetch(item_chunk(p1c.item + 1), wcur ^ 1);
+        } else {  // one buffer: restage in place once every MMA warp is past its previous P1
+          if (wchunk >= 0) {
+            bar_sync(bars::kMma, kGroup);
+            w_fetch(chunk, 0);
+          }
+          cp_async_wait0();
+          bar_sync(bars::kMma, kGroup);
         }
-        bar_sync(bars::kMma, kGroup);
         wchunk = chunk;
       }
-      const XT* xs = xbuf(i);
+      const double* ws = ws_buf(wcur);
+      const XT* xs = xslot(xb);
       const int pt = gwarp & 3, half = gwarp >> 2;
       double c1[kMaxCT][2];
 #pragma unroll
@@ -465,26 +508,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
             make_double2(c1[ct][0], c1[ct][1]);
     };
 
+    if (MODE != kModeInit && !(pa.dbg & 65)) w_fetch(item_chunk(item_begin), 0);  // the first chunk (waited in P1(0))
     for (int f = 0; f < nbuf - 1 && f < ntile; ++f) load_next_x(f);  // X(0 .. nbuf−2) in flight
-    x_wait(0);
-    phase1(0);
-    cursor_next(p1c, d);
+    phase1(0, x_wait());
+    cursor_next(p1c, d, slt);
     s_arrive(0);
     for (int it = 0; it < ntile; ++it) {
       // X(i+nbuf−1) into X(i−1)'s slot (released after P3(i−1)): nbuf−1 tiles of lead
       if (it + nbuf - 1 < ntile) load_next_x(it + nbuf - 1);
       if (it + 1 < ntile) {
         {
+          int xb;
+          {
+            EDAA_TSTART();
+            xb = x_wait();
+            EDAA_TSTOP(0);
+          }
           EDAA_TSTART();
-          x_wait(it + 1);
-          EDAA_TSTOP(0);
-        }
-        {
-          EDAA_TSTART();
-          phase1(it + 1);
+          phase1(it + 1, xb);
           EDAA_TSTOP(1);
         }
-        cursor_next(p1c, d);
+        cursor_next(p1c, d, slt);
         s_arrive(it + 1);
       }
       {
@@ -494,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       }
       if (MODE != kModeObj) {
         if (MODE == kModeB || MODE == kModeInit) {
-          const double* fac = facb + (it & 1) * d.QCpad;
+          const double* fac = facb + (it & 1) * kQMax;
 #pragma unroll
           for (int ct = 0; ct < kMaxCT; ++ct) {
             const double f0 = fac[ct * 8 + 2 * t4], f1 = fac[ct * 8 + 2 * t4 + 1];
@@ -508,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           }
         }
         // P3: C[l][c] += Σ_j X[l][j]·w[c][j]; warp owns row tiles gwarp, gwarp+8, …
-        const XT* xs = xbuf(it);
+        const XT* xs = xslot(p3r.slot);
         const double* w = sbuf(it);
         EDAA_TSTART();
         if (!(pa.dbg & 129)) {
@@ -530,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         }
         EDAA_TSTOP(3);
         if (p3c.tile + 1 == p3c.tend) {  // the item's last tile: flush and restart its partials
-          const int slice = p3c.slice, col0 = p3c.chunk * d.QCpad;
+          const int slice = p3c.slice, col0 = p3c.chunk * kQMax;
 #pragma unroll
           for (int i = 0; i < RTW; ++i) {
             const int rt = gwarp + 8 * i;
@@ -548,21 +592,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           }
         }
       }
-      x_release(it);  // this warp is done with X(i) (P1(i) and P3(i))
-      warp_arrive(sfree + it % d.nsb);  // … and with S(i)/w(i)
-      cursor_next(p3c, d);
+      x_release();  // this warp is done with X(i) (P1(i) and P3(i))
+      warp_arrive(sfree + (it & 1));  // … and with S(i)/w(i)
+      cursor_next(p3c, d, slt);
     }
   } else {
     // ========================== update group ==========================
     Cursor sc, p2c;
-    cursor_set(sc, d, item_begin);
-    cursor_set(p2c, d, item_begin);
+    cursor_set(sc, d, slt, item_begin);
+    cursor_set(p2c, d, slt, item_begin);
     int cchunk = -1;
+    int stl = 0, stu = 0;  // state-tile ring (3 slots): next load, current use
     auto next_state = [&](int f) {  // one commit group per call (empty past the end)
       if (f < ntile) {
         const ChunkInfo cn = chunk_info(d, sc.chunk);
-        issue_state<MODE>(pa, stbuf(f), sc.tile * kNP, cn.srow0, cn.ncol, gtid);
-        cursor_next(sc, d);
+        issue_state<MODE>(pa, stslot(stl), sc.tile * kNP, cn.srow0, cn.ncol, gtid);
+        stl = (stl == 2) ? 0 : stl + 1;
+        cursor_next(sc, d, slt);
       } else {
         cp_async_commit();
       }
@@ -579,12 +625,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     for (int it = 0; it < ntile; ++it) {
       const ChunkInfo ci = chunk_info(d, p2c.chunk);
       const int j0 = p2c.tile * kNP;
-      const bool item_first = p2c.tile == slice_tile(d, p2c.slice);
+      const bool item_first = p2c.tile == p2c.tstart;
       const bool item_last = p2c.tile + 1 == p2c.tend;
       bar_sync(bars::kUpd, kGroup);  // everyone is done with st(i−1) and the previous item's scalars
       next_state(it + 2);            // into st(i−1)'s slot
       if (ci.chunk != cchunk) {  // per-column constants and G blocks of the new chunk
-        if (gtid < d.QCpad) {
+        if (gtid < kQMax) {
           const int c = gtid;
           const bool real = c < ci.ncol;
           // log b_old = ℓ − (m + log S): one subtraction per element
@@ -601,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         cchunk = ci.chunk;
       }
       if (item_first) {
-        if (gtid < d.QCpad) {
+        if (gtid < kQMax) {
           m_run[gtid] = -INFINITY;
           S_run[gtid] = 0.0;
         }
@@ -617,8 +663,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       EDAA_TSTART();
       double* ss = sbuf(it);
       const double* sh = hbuf(it);
-      const double* st = stbuf(it);
-      double* fac = facb + (it & 1) * d.QCpad;
+      const double* st = stslot(stu);
+      stu = (stu == 2) ? 0 : stu + 1;
+      double* fac = facb + (it & 1) * kQMax;
 
       if (MODE == kModeA || MODE == kModeObj) {
         constexpr int TPP = LanesPerPixel<PT>::value;
@@ -635,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           if (lane == 0) hobj[q2 >> 5] = o;  // warp-task q2/32 belongs to run (q2/32)/TPP
         }
         if (MODE == kModeA)
-          for (int e = gtid; e < (d.QCpad - ci.ncol) * kNP; e += kGroup)
+          for (int e = gtid; e < (kQMax - ci.ncol) * kNP; e += kGroup)
             ss[(ci.ncol + e / kNP) * kSST + e % kNP] = 0.0;
         bar_sync(bars::kUpd, kGroup);
         if (gtid < ci.RCe) {
@@ -646,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       } else if (!(pa.dbg & 2)) {
         // B step / B⁰: new logits; 8 lanes per column, 4 pixels per lane (j = k·8 + lane8).
         const int c = gtid >> 3, l8 = gtid & 7;
-        const bool active = c < d.QCpad;  // QCpad·8 ≤ 192 threads carry columns
+        const bool active = c < kQMax;  // QCpad·8 ≤ 192 threads carry columns
         double ell[4];
         double tmax = -INFINITY;
         if (active) {
@@ -700,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         bar_sync(bars::kUpd, kGroup);
         const int slice = p2c.slice;
         if (MODE == kModeB || MODE == kModeInit) {
-          if (gtid < d.QCpad) {
+          if (gtid < kQMax) {
             pa.part_m[static_cast<size_t>(slice) * d.Qs + ci.col0 + gtid] = m_run[gtid];
             pa.part_S[static_cast<size_t>(slice) * d.Qs + ci.col0 + gtid] = S_run[gtid];
           }
@@ -709,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         }
       }
       w_arrive(it);  // w(i), fac(i) ready for P3(i)
-      cursor_next(p2c, d);
+      cursor_next(p2c, d, slt);
     }
   }
 }
@@ -745,7 +792,7 @@ cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
 template <class XT>
 cudaError_t launch_pass_xt(int mode, const PassArgs& a, cudaStream_t st) {
   const int pt = pt_bucket(a.d.p);
-  const bool wide = (a.d.Lpad / 8 + a.d.QCpad / 8) > 32;  // > 4 row tiles per warp
+  const bool wide = (a.d.Lpad / 8 + kQMax / 8) > 32;  // > 4 row tiles per warp
   switch (mode) {
     case kModeInit:
       return wide ? launch_pass_rtw<kModeInit, 6, XT>(a, st, pt) : launch_pass_rtw<kModeInit, 4, XT>(a, st, pt);

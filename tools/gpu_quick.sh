@@ -8,3 +8,4 @@ for f in ["b1","b_cfg2","b_cfg3"]:
         d=json.load(open("gpurun_out/"+f+".json")); print(f, round(d["value"],1), round(d["ms_per_step"],1), round(d["roofline"]["frac"],3), {k: round(v,1) for k,v in d["roofline"]["pass_ms"].items()})
     except Exception as e: print(f, e, open("gpurun_out/"+f+".json").read()[-2000:])
 PY
+bash tools/kprof.sh "cfg1 cfg2" 2>&1 | grep -v DBG=2 | tail -6
