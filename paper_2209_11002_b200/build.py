@@ -24,8 +24,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                   "-I" + os.path.join(ROOT, "include")]
-CUDA_SRCS = ["edaa_pass_f32.cu", "edaa_pass_f64.cu", "edaa_kernels.cu", "edaa_prims.cu",
-             "edaa_capi.cu"]
+CUDA_SRCS = (["edaa_pass_%s_%s.cu" % (x, m) for x in ("f32", "f64") for m in ("alo", "ahi", "b", "init", "obj")]
+             + ["edaa_kernels.cu", "edaa_prims.cu", "edaa_capi.cu"])
 HOST_SRCS = ["matrix.cpp", "image.cpp", "types.cpp", "solver.cpp", "ensemble.cpp", "device.cpp"]
 
 CUDA_LIB = os.path.join(PKG, "libedaa_cuda.so")
@@ -57,7 +57,7 @@ def build_cuda(force=False, verbose=False):
         objs.append(obj)
         if force or _stale(obj, [src] + hdrs):
             jobs.append([NVCC] + NVFLAGS + ["-c", src, "-o", obj])
-    with cf.ThreadPoolExecutor(max_workers=4) as ex:
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         for out in ex.map(_run, jobs):
             if verbose and out:
                 print(out)

@@ -338,11 +338,28 @@ __global__ void k_select(const double* fit, const double* mu, const int* fail_co
 
 size_t pass_smem_bytes(const Dims& d, int nbuf) { return dev::smem_layout(d, nbuf).total; }
 
-cudaError_t launch_pass_f32(int mode, const PassArgs& a, cudaStream_t st);
-cudaError_t launch_pass_f64(int mode, const PassArgs& a, cudaStream_t st);
+#define EDAA_DECL_PASS(X)                                             \
+  cudaError_t launch_pass_##X##_init(const PassArgs&, cudaStream_t); \
+  cudaError_t launch_pass_##X##_b(const PassArgs&, cudaStream_t);    \
+  cudaError_t launch_pass_##X##_obj(const PassArgs&, cudaStream_t);  \
+  cudaError_t launch_pass_##X##_alo(const PassArgs&, cudaStream_t);  \
+  cudaError_t launch_pass_##X##_ahi(const PassArgs&, cudaStream_t);
+EDAA_DECL_PASS(f32)
+EDAA_DECL_PASS(f64)
+#undef EDAA_DECL_PASS
 
 cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st) {
-  return a.d.xbytes == 8 ? launch_pass_f64(mode, a, st) : launch_pass_f32(mode, a, st);
+  const bool f64 = a.d.xbytes == 8;
+  const bool lo = a.d.p <= 5;
+  switch (mode) {
+    case kModeInit: return f64 ? launch_pass_f64_init(a, st) : launch_pass_f32_init(a, st);
+    case kModeB: return f64 ? launch_pass_f64_b(a, st) : launch_pass_f32_b(a, st);
+    case kModeObj: return f64 ? launch_pass_f64_obj(a, st) : launch_pass_f32_obj(a, st);
+    case kModeA:
+      if (f64) return lo ? launch_pass_f64_alo(a, st) : launch_pass_f64_ahi(a, st);
+      return lo ? launch_pass_f32_alo(a, st) : launch_pass_f32_ahi(a, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 

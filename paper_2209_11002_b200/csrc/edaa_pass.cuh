@@ -761,25 +761,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   }
 }
 
-template <int MODE, int RTW, class XT>
+// PTS selects the p buckets this instantiation carries (kPtAll, kPtLo = 2-5,
+// kPtHi = 6-16): a template parameter, not a macro, so translation units that
+// carry different bucket sets never define the same function differently.
+enum PtSet : int { kPtAll = 0, kPtLo = 1, kPtHi = 2 };
+
+template <int MODE, int RTW, class XT, int PTS>
 cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
   const dim3 grid(std::min(a.d.NCH * a.d.nslices, a.d.ncta));
   const size_t smem = dev::smem_layout(a.d, a.d.nbuf).total;
   void (*kern)(PassArgs, CUtensorMap) = nullptr;
-  if (MODE == kModeInit || MODE == kModeB) {
+  if constexpr (MODE == kModeInit || MODE == kModeB) {
     kern = k_pass<MODE, 1, RTW, XT>;
   } else {
     switch (pt) {
-#define EDAA_PT_CASE(P)                                       \
-  case P:                                                     \
-    kern = k_pass<MODE, P, RTW, XT>;                          \
+#define EDAA_PT_CASE(P)                                                                     \
+  case P:                                                                                   \
+    if constexpr (PTS == kPtAll || (PTS == kPtLo) == (P <= 5)) kern = k_pass<MODE, P, RTW, XT>; \
     break;
-      EDAA_PT_CASE(2) EDAA_PT_CASE(3) EDAA_PT_CASE(4) EDAA_PT_CASE(5) EDAA_PT_CASE(6)
-      EDAA_PT_CASE(7) EDAA_PT_CASE(8) EDAA_PT_CASE(10) EDAA_PT_CASE(12) EDAA_PT_CASE(16)
+      EDAA_PT_CASE(2) EDAA_PT_CASE(3) EDAA_PT_CASE(4) EDAA_PT_CASE(5)
+      EDAA_PT_CASE(6) EDAA_PT_CASE(7) EDAA_PT_CASE(8) EDAA_PT_CASE(10) EDAA_PT_CASE(12) EDAA_PT_CASE(16)
 #undef EDAA_PT_CASE
       default:
-        return cudaErrorInvalidValue;
+        break;
     }
+    if (kern == nullptr) return cudaErrorInvalidValue;
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -789,23 +795,18 @@ cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
 }
 
 
-template <class XT>
-cudaError_t launch_pass_xt(int mode, const PassArgs& a, cudaStream_t st) {
+// Per-mode entry points: each translation unit edaa_pass_<x>_<part>.cu instantiates
+// one (image type, mode, p-bucket range) so the kernels compile in parallel.
+template <int MODE, class XT, int PTS = kPtAll>
+cudaError_t launch_pass_mode(const PassArgs& a, cudaStream_t st) {
   const int pt = pt_bucket(a.d.p);
   const bool wide = (a.d.Lpad / 8 + kQMax / 8) > 32;  // > 4 row tiles per warp
-  switch (mode) {
-    case kModeInit:
-      return wide ? launch_pass_rtw<kModeInit, 6, XT>(a, st, pt) : launch_pass_rtw<kModeInit, 4, XT>(a, st, pt);
-    case kModeA:
-      return wide ? launch_pass_rtw<kModeA, 6, XT>(a, st, pt) : launch_pass_rtw<kModeA, 4, XT>(a, st, pt);
-    case kModeB:
-      return wide ? launch_pass_rtw<kModeB, 6, XT>(a, st, pt) : launch_pass_rtw<kModeB, 4, XT>(a, st, pt);
-    case kModeObj:
-      return launch_pass_rtw<kModeObj, 1, XT>(a, st, pt);
+  if constexpr (MODE == kModeObj) {
+    return launch_pass_rtw<kModeObj, 1, XT, PTS>(a, st, pt);
+  } else {
+    return wide ? launch_pass_rtw<MODE, 6, XT, PTS>(a, st, pt) : launch_pass_rtw<MODE, 4, XT, PTS>(a, st, pt);
   }
-  return cudaErrorInvalidValue;
 }
-
 
 }  // namespace pass_impl
 }  // namespace edaa

@@ -1,0 +1,9 @@
+// Pass-kernel instantiations: float image, kModeB.
+// (One translation unit per mode so the kernels compile in parallel.)
+#include "edaa_pass.cuh"
+
+namespace edaa {
+cudaError_t launch_pass_f32_b(const PassArgs& a, cudaStream_t st) {
+  return pass_impl::launch_pass_mode<kModeB, float>(a, st);
+}
+}  // namespace edaa
