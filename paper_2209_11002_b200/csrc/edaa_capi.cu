@@ -326,6 +326,7 @@ edaa::CombineArgs combine_args(edaa_ctx* c, int t, int mode, int trace_index) {
   a.fac = P<double>(c->fac);
   a.XAt = P<double>(c->XAt);
   a.AAt = P<double>(c->AAt);
+  a.Z = (mode == edaa::kModeA || mode == edaa::kModeB) ? P<double>(c->Z) : nullptr;
   a.trace = P<double>(c->trace);
   a.trace_stride = static_cast<int>(c->T + 1);
   a.trace_index = trace_index;
@@ -494,8 +495,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
     if (hook) pa.observe_A = P<double>(c->obsA);
     rc = launch_pass_profiled(c, edaa::kModeA, pa);
     if (rc) return rc;
-    EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeA, ti - 1), st));
-    EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostZ), st));
+    EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeA, ti - 1), st), 2);
     if (hook) {
       // B is fixed through the A block; snapshot it once, then replay the K1 iterates.
       rc = download_b(c, hook);
@@ -517,8 +517,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
       rc = launch_pass_profiled(c, edaa::kModeB, pb);
       if (rc) return rc;
       EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0), st), 2);
-      const bool last = (k == prm->inner_iters_b);
-      EDAA_LAUNCH(c, edaa::launch_post(post_args(c, last ? edaa::kPostG : edaa::kPostZ), st));
+      if (k == prm->inner_iters_b) EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostG), st));
       if (hook) {
         rc = download_b(c, hook);
         if (rc) return rc;

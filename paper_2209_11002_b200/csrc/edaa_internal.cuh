@@ -28,8 +28,8 @@ constexpr int kXST = kNP + 8;   // fp32 X tile row stride (conflict-free DMMA B-
 constexpr int kSST = kNP + 4;   // fp64 weight tile row stride
 constexpr int kQMax = 24;       // columns per chunk (3 DMMA column tiles)
 constexpr int kMaxCT = kQMax / 8;
-constexpr int kMaxSlices = 296; // 2 × 148 SMs
-constexpr int kTilesPerSlice = 8;
+constexpr int kMaxSlices = 148; // bounds the slice-partial traffic (nslices·(L+24)·Q doubles per pass)
+constexpr int kTilesPerSlice = 4;  // 128-pixel slices: ~5 (slice, chunk) items per CTA at cfg1
 constexpr int kMaxP = 16;
 constexpr int kMaxLpad = 320;
 constexpr double kLogFloorValue = 1e-30;  // solver.cpp:15
@@ -97,7 +97,8 @@ struct CombineArgs {
   double* collogS;
   double* fac;      // [nslices][Qs] scratch: exp(m_s − m) per slice and column
   double* XAt;      // A output
-  double* AAt;      // A output [QCpad][Qs]
+  double* AAt;      // A output [QCpad][Qs] (run-diagonal p×p blocks)
+  double* Z;        // A/B output: Z = XAᵀ − Y·AAᵀ (nullptr: not formed, init)
   double* trace;    // [M][T+1]
   int trace_stride;
   int trace_index;

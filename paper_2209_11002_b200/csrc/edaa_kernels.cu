@@ -96,6 +96,110 @@ __global__ void k_rowsum(CombineArgs ca, int rows) {
 }
 
 // ---------------------------------------------------------------------------
+// Combine of one pass's slice partials, fused with Z = XAᵀ − Y·AAᵀ
+// (solver.cpp:221, anchored on the A block's XAᵀ/AAᵀ).  One CTA per (run
+// chunk, kCR band rows); 256 threads = kCR rows × kCG slice groups × 32 lanes
+// (lane x < kQMax = column of the chunk).  Group g sums the contiguous slice
+// range [g·S/kCG, (g+1)·S/kCG) in ascending order and the kCG group sums are
+// added in g order: one fixed order that depends on the slicing (a function of
+// N) only, so a run's arithmetic stays independent of its batch and position
+// (test_ensemble.cpp:150-169 analogue).
+//   B / init: Y rows = Σ_s C_s·e^{m_s−m} / S (fac, S from k_colnorm), then Z;
+//   A:        XAᵀ rows = Σ_s C_s, then Z with the block's Y and AAᵀ (k_aat).
+constexpr int kCR = 2;
+constexpr int kCG = 4;
+
+__global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
+  __shared__ double red[kCR * kCG][kQMax];
+  __shared__ double ys[kCR][kQMax];
+  const Dims& d = ca.d;
+  const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
+  const int rr = y % kCR, g = y / kCR;
+  const int col0 = blockIdx.x * d.QCpad;
+  const int S = d.nslices;
+  const int p = d.p;
+  const int ncol = min(d.RC, d.M - static_cast<int>(blockIdx.x) * d.RC) * p;
+  const bool lse = (ca.mode == kModeB || ca.mode == kModeInit);
+  const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
+  const int l = blockIdx.y * kCR + rr;
+  const bool live = (x < kQMax) && (l < d.Lpad);
+  if (live) {
+    const int s0 = (g * S) / kCG, s1 = ((g + 1) * S) / kCG;
+    const double* src = ca.part_C + static_cast<size_t>(l) * d.Qs + col0 + x;
+    double v = 0.0;
+    if (lse) {
+      const double* f = ca.fac + col0 + x;
+#pragma unroll 8
+      for (int sl = s0; sl < s1; ++sl) v += src[sl * sstride] * f[static_cast<size_t>(sl) * d.Qs];
+    } else {
+#pragma unroll 8
+      for (int sl = s0; sl < s1; ++sl) v += src[sl * sstride];
+    }
+    red[y][x] = v;
+  }
+  __syncthreads();
+  if (g == 0 && live) {
+    double v = red[rr][x];
+    for (int k = 1; k < kCG; ++k) v += red[k * kCR + rr][x];
+    const size_t o = static_cast<size_t>(l) * d.Qs + col0 + x;
+    if (lse) {
+      v = (x < ncol) ? v / ca.colS[col0 + x] : 0.0;  // padding columns carry no run
+      ca.Y[o] = v;
+      ys[rr][x] = v;
+    } else {
+      ca.XAt[o] = v;
+      red[rr][x] = v;
+      ys[rr][x] = ca.Y[o];
+    }
+  }
+  if (ca.Z == nullptr) return;
+  __syncthreads();
+  if (g == 0 && live && x < ncol) {
+    // Z = XAᵀ − Y·AAᵀ for this row (m ascending, from 0)
+    const int rl = x / p;
+    const double* arow = ca.AAt + static_cast<size_t>(rl * p) * d.Qs + col0 + x;  // AAᵀ[rl·p+m][x]
+    double sacc = 0.0;
+    for (int mm = 0; mm < p; ++mm) sacc += ys[rr][rl * p + mm] * arow[static_cast<size_t>(mm) * d.Qs];
+    const size_t o = static_cast<size_t>(l) * d.Qs + col0 + x;
+    const double xa = lse ? ca.XAt[o] : red[rr][x];
+    ca.Z[o] = xa - sacc;
+  }
+}
+
+// A block: the run-diagonal AAᵀ blocks (pseudo-band rows Lpad + rl·p + i of the
+// slice partials) and, from CTA 0, the objective trace; one CTA per chunk.
+// Same fixed slice order as k_combine (contiguous groups, then group order).
+__global__ void __launch_bounds__(256) k_aat(CombineArgs ca) {
+  const Dims& d = ca.d;
+  const int S = d.nslices;
+  const int p = d.p;
+  const int col0 = blockIdx.x * d.QCpad;
+  const int RCe = min(d.RC, d.M - static_cast<int>(blockIdx.x) * d.RC);
+  const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
+  for (int e = threadIdx.x; e < RCe * p * p; e += blockDim.x) {
+    const int rl = e / (p * p), rem = e - rl * p * p;
+    const int i = rem / p, mcol = rem - i * p;
+    const double* src = ca.part_C + static_cast<size_t>(d.Lpad + rl * p + i) * d.Qs + col0 + rl * p + mcol;
+    double tot = 0.0;
+    for (int g = 0; g < kCG; ++g) {
+      double v = 0.0;
+#pragma unroll 8
+      for (int sl = (g * S) / kCG; sl < ((g + 1) * S) / kCG; ++sl) v += src[sl * sstride];
+      tot = (g == 0) ? v : tot + v;
+    }
+    ca.AAt[static_cast<size_t>(rl * p + i) * d.Qs + col0 + rl * p + mcol] = tot;
+  }
+  if (blockIdx.x == 0) {
+    for (int r = threadIdx.x; r < d.M; r += blockDim.x) {
+      double o = 0.0;
+#pragma unroll 8
+      for (int sl = 0; sl < S; ++sl) o += ca.part_obj[static_cast<size_t>(sl) * d.M + r];
+      ca.trace[static_cast<size_t>(r) * ca.trace_stride + ca.trace_index] = o;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Per-run small algebra: Z = XAᵀ − Y·AAᵀ, G = YᵀY, and (init) the step sizes.
 __global__ void __launch_bounds__(256) k_post(PostArgs pa) {
   const Dims& d = pa.d;
@@ -365,14 +469,17 @@ cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st) {
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   const Dims& d = a.d;
-  if (a.mode == kModeB || a.mode == kModeInit) {
-    k_colnorm<<<(d.Qs + 7) / 8, 256, 0, st>>>(a);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+  if (a.mode == kModeObj) {  // the final objective only
+    k_rowsum<<<dim3((d.Qs + 31) / 32, 1), dim3(32, 8), 0, st>>>(a, 0);
+    return cudaGetLastError();
   }
-  const int rows = (a.mode == kModeA) ? d.Lrows : (a.mode == kModeObj ? 0 : d.Lpad);
-  const dim3 grid((d.Qs + 31) / 32, rows > 0 ? (rows + 7) / 8 : 1);
-  k_rowsum<<<grid, dim3(32, 8), 0, st>>>(a, rows);
+  if (a.mode == kModeA)
+    k_aat<<<d.NCH, 256, 0, st>>>(a);
+  else
+    k_colnorm<<<(d.Qs + 7) / 8, 256, 0, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_combine<<<dim3(d.NCH, (d.Lpad + kCR - 1) / kCR), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
