@@ -167,35 +167,56 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
 }
 
 // A block: the run-diagonal AAᵀ blocks (pseudo-band rows Lpad + rl·p + i of the
-// slice partials) and, from CTA 0, the objective trace; one CTA per chunk.
-// Same fixed slice order as k_combine (contiguous groups, then group order).
+// slice partials) and the objective trace.  One warp per output: lane k sums
+// the contiguous slice range [k·S/32, (k+1)·S/32) in ascending order, then a
+// fixed xor tree — an order that depends on the slicing only.
+// grid = (NCH, ⌈RC·p²/8⌉ + 1): the last y-row of CTAs folds the traces.
 __global__ void __launch_bounds__(256) k_aat(CombineArgs ca) {
   const Dims& d = ca.d;
   const int S = d.nslices;
   const int p = d.p;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s0 = (lane * S) / 32, s1 = ((lane + 1) * S) / 32;
+  if (blockIdx.y + 1 == gridDim.y) {  // traces: runs r ≡ (blockIdx.x·8 + w) mod (NCH·8)
+    for (int r = blockIdx.x * 8 + w; r < d.M; r += gridDim.x * 8) {
+      double o = 0.0;
+      for (int sl = s0; sl < s1; ++sl) o += ca.part_obj[static_cast<size_t>(sl) * d.M + r];
+      o = warp_sum(o);
+      if (lane == 0) ca.trace[static_cast<size_t>(r) * ca.trace_stride + ca.trace_index] = o;
+    }
+    return;
+  }
   const int col0 = blockIdx.x * d.QCpad;
   const int RCe = min(d.RC, d.M - static_cast<int>(blockIdx.x) * d.RC);
+  const int e = blockIdx.y * 8 + w;
+  if (e >= RCe * p * p) return;
+  const int rl = e / (p * p), rem = e - rl * p * p;
+  const int i = rem / p, mcol = rem - i * p;
   const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
-  for (int e = threadIdx.x; e < RCe * p * p; e += blockDim.x) {
-    const int rl = e / (p * p), rem = e - rl * p * p;
-    const int i = rem / p, mcol = rem - i * p;
-    const double* src = ca.part_C + static_cast<size_t>(d.Lpad + rl * p + i) * d.Qs + col0 + rl * p + mcol;
-    double tot = 0.0;
-    for (int g = 0; g < kCG; ++g) {
-      double v = 0.0;
-#pragma unroll 8
-      for (int sl = (g * S) / kCG; sl < ((g + 1) * S) / kCG; ++sl) v += src[sl * sstride];
-      tot = (g == 0) ? v : tot + v;
-    }
-    ca.AAt[static_cast<size_t>(rl * p + i) * d.Qs + col0 + rl * p + mcol] = tot;
-  }
-  if (blockIdx.x == 0) {
-    for (int r = threadIdx.x; r < d.M; r += blockDim.x) {
-      double o = 0.0;
-#pragma unroll 8
-      for (int sl = 0; sl < S; ++sl) o += ca.part_obj[static_cast<size_t>(sl) * d.M + r];
-      ca.trace[static_cast<size_t>(r) * ca.trace_stride + ca.trace_index] = o;
-    }
+  const double* src = ca.part_C + static_cast<size_t>(d.Lpad + rl * p + i) * d.Qs + col0 + rl * p + mcol;
+  double v = 0.0;
+  for (int sl = s0; sl < s1; ++sl) v += src[sl * sstride];
+  v = warp_sum(v);
+  if (lane == 0) ca.AAt[static_cast<size_t>(rl * p + i) * d.Qs + col0 + rl * p + mcol] = v;
+}
+
+// G = YᵀY per run for the next A block (p×p, one warp per entry: lanes stride
+// the bands, fixed xor tree).  The init Gram that feeds step_sizes keeps the
+// reference's band-ascending order in k_post.
+__global__ void __launch_bounds__(256) k_gram(PostArgs pa) {
+  const Dims& d = pa.d;
+  const int r = blockIdx.x;
+  const int p = d.p;
+  const int c0 = (r / d.RC) * d.QCpad + (r % d.RC) * p;
+  const int lr0 = (r % d.RC) * p;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int e = w; e < p * p; e += 8) {
+    const int i = e / p, m = e - i * p;
+    double s = 0.0;
+    for (int l = lane; l < d.L; l += 32)
+      s += pa.Y[static_cast<size_t>(l) * d.Qs + c0 + i] * pa.Y[static_cast<size_t>(l) * d.Qs + c0 + m];
+    s = warp_sum(s);
+    if (lane == 0) pa.Gbuf[static_cast<size_t>(lr0 + i) * d.Qs + c0 + m] = s;
   }
 }
 
@@ -320,37 +341,40 @@ __global__ void k_materialize_b(const double* Lg, const double* colm, const doub
 // matmul(X, B̂) of the same fp32-exact X. Output [M][Lpad][p].
 template <class XT>
 __global__ void __launch_bounds__(256) k_strict_e(const XT* X, const double* Bv, double* E, Dims d) {
-  __shared__ double xs[32][65];
+  // One output per thread (8 band rows × 32 columns per CTA): the pixel-ascending
+  // chain is inherently sequential, so throughput comes from running many chains
+  // (L·M·p of them) on every SM at once.
+  __shared__ double xs[8][64];
   __shared__ double bs[32][65];
   const int lane = threadIdx.x & 31, ry = threadIdx.x >> 5;
-  const int l0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int l0 = blockIdx.x * 8, c0 = blockIdx.y * 32;
   const int ncol = d.M * d.p;
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  double s = 0.0;
   for (int j0 = 0; j0 < d.N; j0 += 64) {
+    for (int e = threadIdx.x; e < 8 * 64; e += 256) {
+      const int rr = e / 64, jj = e % 64;
+      const int l = l0 + rr, j = j0 + jj;
+      xs[rr][jj] = (l < d.L && j < d.N) ? static_cast<double>(X[static_cast<size_t>(l) * d.Npad + j]) : 0.0;
+    }
     for (int e = threadIdx.x; e < 32 * 64; e += 256) {
       const int rr = e / 64, jj = e % 64;
-      const int l = l0 + rr, c = c0 + rr, j = j0 + jj;
-      xs[rr][jj] = (l < d.L && j < d.N) ? static_cast<double>(X[static_cast<size_t>(l) * d.Npad + j]) : 0.0;
+      const int c = c0 + rr, j = j0 + jj;
       bs[rr][jj] = (c < ncol && j < d.N) ? Bv[static_cast<size_t>(c) * d.Npad + j] : 0.0;
     }
     __syncthreads();
-    const int jn = min(64, d.N - j0);
-    for (int jj = 0; jj < jn; ++jj) {
-      const double b = bs[lane][jj];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        s[q] = __dadd_rn(s[q], __dmul_rn(static_cast<double>(xs[ry + 8 * q][jj]), b));
+    if (d.N - j0 >= 64) {
+#pragma unroll 16
+      for (int jj = 0; jj < 64; ++jj) s = __dadd_rn(s, __dmul_rn(xs[ry][jj], bs[lane][jj]));
+    } else {
+      for (int jj = 0; jj < d.N - j0; ++jj) s = __dadd_rn(s, __dmul_rn(xs[ry][jj], bs[lane][jj]));
     }
     __syncthreads();
   }
   const int c = c0 + lane;
-  if (c >= ncol) return;
+  const int l = l0 + ry;
+  if (c >= ncol || l >= d.L) return;
   const int r = c / d.p, i = c % d.p;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int l = l0 + ry + 8 * q;
-    if (l < d.L) E[(static_cast<size_t>(r) * d.Lpad + l) * d.p + i] = s[q];
-  }
+  E[(static_cast<size_t>(r) * d.Lpad + l) * d.p + i] = s;
 }
 
 // fit_l1 = Σ |X − E·A| (ensemble.cpp:29-39). Per element the reconstruction
@@ -474,7 +498,7 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
     return cudaGetLastError();
   }
   if (a.mode == kModeA)
-    k_aat<<<d.NCH, 256, 0, st>>>(a);
+    k_aat<<<dim3(d.NCH, (d.RC * d.p * d.p + 7) / 8 + 1), 256, 0, st>>>(a);
   else
     k_colnorm<<<(d.Qs + 7) / 8, 256, 0, st>>>(a);
   cudaError_t e = cudaGetLastError();
@@ -484,7 +508,10 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_post(const PostArgs& a, cudaStream_t st) {
-  k_post<<<a.d.M, 256, 0, st>>>(a);
+  if (a.mode == kPostG)
+    k_gram<<<a.d.M, 256, 0, st>>>(a);
+  else
+    k_post<<<a.d.M, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -505,7 +532,7 @@ cudaError_t launch_materialize_b(const double* Lg, const double* colm, const dou
 
 cudaError_t launch_strict_e(const void* X, const double* Bv, double* E, const Dims& d,
                             cudaStream_t st) {
-  const dim3 grid((d.L + 31) / 32, (d.M * d.p + 31) / 32);
+  const dim3 grid((d.L + 7) / 8, (d.M * d.p + 31) / 32);
   if (d.xbytes == 8)
     k_strict_e<<<grid, 256, 0, st>>>(static_cast<const double*>(X), Bv, E, d);
   else
