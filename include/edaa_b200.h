@@ -124,6 +124,28 @@ typedef void (*edaa_observer_fn)(size_t outer, char block, size_t inner, const d
 EDAA_API int edaa_solve_observed(edaa_ctx* ctx, const edaa_solve_params* params, edaa_observer_fn fn,
                         void* user);
 
+/* Pixel sharding of one solve over the GPUs of a node (no
+ * reference counterpart — the reference runs a solve on one host thread,
+ * solver.cpp:190-238).  One context per GPU, one process (or thread) per
+ * context.  Rank 0 makes a communicator id with edaa_nccl_unique_id and sends
+ * its bytes to every rank out of band (torch.distributed in
+ * paper_2209_11002_b200/distributed.py); every rank then calls
+ * edaa_set_pixel_shard with the same id (collective: blocks until all world
+ * ranks joined).  From then on each solve on the context processes only the
+ * rank's pixel slices and exchanges the slice partials after every pass
+ * (NCCL broadcasts, inside the captured CUDA graph), so every rank ends with
+ * the full result, bitwise equal to the one-device solve.  id == NULL turns
+ * sharding off (world == 1 with an id makes a one-rank communicator whose
+ * exchanges run as a self-check).  NCCL (libnccl.so.2) is resolved at run time.
+ * edaa_shard_pixels: the pixel range [first, end) this rank owns in the last
+ * solve.  edaa_set_shard_emulation(ctx, W): development/test mode on ONE
+ * device — every pass is launched as W consecutive slice-range launches (no
+ * collective), which checks the sharded decomposition without more GPUs. */
+EDAA_API int edaa_nccl_unique_id(void* out, size_t bytes /* >= 128 */);
+EDAA_API int edaa_set_pixel_shard(edaa_ctx* ctx, const void* id, size_t bytes, int rank, int world);
+EDAA_API int edaa_shard_pixels(edaa_ctx* ctx, size_t* first, size_t* end);
+EDAA_API int edaa_set_shard_emulation(edaa_ctx* ctx, int world);
+
 /* Single-evaluation primitives on the image of the context (reference
  * solver.hpp:52-67,85-86 and ensemble.hpp:50).  Host arrays in the
  * reference layouts (b: N×p, a: p×N, e: L×p); entries follow the reference's

@@ -15,9 +15,12 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include <cuda.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include "../../include/edaa_b200.h"
 #include "edaa_device.cuh"
@@ -28,6 +31,8 @@ struct GraphKey {
   Dims d;
   size_t T, K2;
   uint64_t gen;
+  const void* comm;
+  int emulate;
 };
 
 struct edaa_ctx {
@@ -74,6 +79,10 @@ struct edaa_ctx {
   std::vector<double> h_fit, h_mu, h_eta_a, h_eta_b, h_fail_value, h_trace;
   std::vector<int> h_fail_code;
   std::vector<unsigned long long> h_fail_key;
+  // pixel sharding of one solve over the GPUs of a node (NCCL communicator; world 1 = off)
+  ncclComm_t comm = nullptr;
+  int shard_rank = 0, shard_world = 1;
+  int shard_emulate = 0;  // > 1: run the slice ranges of that many ranks one after another here
 };
 
 namespace {
@@ -170,6 +179,72 @@ std::string run_message(int code, size_t outer, double value) {
   }
 }
 
+// ---- NCCL, resolved at run time (libnccl.so.2: the one already loaded into the
+// process, e.g. by torch, else the system copy) so the library links without it.
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    // EDAA_NCCL_LIB, else the copy already in the process (a host that loads its own
+    // NCCL — torch — must do so first: a later load by soname would bind to ours).
+    void* h = nullptr;
+    if (const char* path = std::getenv("EDAA_NCCL_LIB")) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = "libnccl.so.2 not found";
+      return a;
+    }
+    bool all = true;
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      all &= fn != nullptr;
+    };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.Broadcast, "ncclBroadcast");
+    sym(a.AllReduce, "ncclAllReduce");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    a.ok = all;
+    if (!all) a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+#define EDAA_NCCL(ctx, call)                                                                     \
+  do {                                                                                           \
+    ncclResult_t r_ = (call);                                                                    \
+    if (r_ != ncclSuccess)                                                                       \
+      return set_err((ctx), EDAA_ERR_CUDA, std::string(#call ": ") + nccl().GetErrorString(r_)); \
+  } while (0)
+
+// Slice range [sl0, sl1) of `rank` among `world` (slice boundaries depend on N only).
+void shard_slices(const Dims& d, int rank, int world, int* sl0, int* sl1) {
+  *sl0 = static_cast<int>((static_cast<long long>(rank) * d.nslices) / world);
+  *sl1 = static_cast<int>((static_cast<long long>(rank + 1) * d.nslices) / world);
+}
+// Pixel range of a slice range (tile-aligned; the last slice ends at Npad).
+void slice_pixels(const Dims& d, int sl0, int sl1, int* j0, int* j1) {
+  *j0 = static_cast<int>((static_cast<long long>(sl0) * d.ntiles) / d.nslices) * edaa::kNP;
+  *j1 = static_cast<int>((static_cast<long long>(sl1) * d.ntiles) / d.nslices) * edaa::kNP;
+}
+
 int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   if (!prm || !prm->seeds || !prm->gammas) return set_err(c, EDAA_ERR_INVALID, "null params");
   if (c->X == nullptr) return set_err(c, EDAA_ERR_STATE, "no image set");
@@ -193,6 +268,13 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.Npad = c->Npad;
   d.ntiles = d.Npad / edaa::kNP;
   d.nslices = std::min(edaa::kMaxSlices, (d.ntiles + edaa::kTilesPerSlice - 1) / edaa::kTilesPerSlice);
+  d.sl0 = 0;
+  d.sl1 = d.nslices;
+  if (c->shard_world > 1) {
+    if (d.nslices < c->shard_world)
+      return set_err(c, EDAA_ERR_UNSUPPORTED, "image too small to shard its pixels over that many devices");
+    shard_slices(d, c->shard_rank, c->shard_world, &d.sl0, &d.sl1);
+  }
   d.M = static_cast<int>(prm->runs);
   d.p = static_cast<int>(p);
   d.RC = std::max(1, std::min(edaa::kQMax / d.p, d.M));
@@ -415,6 +497,8 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   Dims d{};
   int rc = make_dims(c, prm, &d);
   if (rc) return rc;
+  if (hook && (c->comm || c->shard_emulate > 1))
+    return set_err(c, EDAA_ERR_UNSUPPORTED, "observed solves are not pixel-sharded");
   c->d = d;
   c->T = prm->outer_iters;
   c->solved = false;
@@ -433,6 +517,8 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   key.T = c->T;
   key.K2 = prm->inner_iters_b;
   key.gen = c->gen;
+  key.comm = c->comm;
+  key.emulate = c->shard_emulate;
   if (!(c->graph_exec && std::memcmp(&key, &c->graph_key, sizeof key) == 0)) {
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     c->graph_exec = nullptr;
@@ -456,6 +542,79 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   EDAA_CUDA(c, cudaGraphLaunch(c->graph_exec, st));
   c->launches += c->graph_launches;
   return EDAA_OK;
+}
+
+// Pixel sharding: after every pass each rank broadcasts the partials of the
+// slices it owns (in place, every rank a root once), so every rank then runs
+// the unchanged fixed-order combine over all slices — the sharded solve is
+// bitwise the single-device solve.  Messages per pass ≈ nslices·(L+24)·Q·8 B
+// in total (A/B) or nslices·M·8 B (objective).
+int exchange_partials(edaa_ctx* c, int mode) {
+  const Dims& d = c->d;
+  const NcclApi& n = nccl();
+  const size_t cblk = static_cast<size_t>(d.Lrows) * d.Qs;
+  EDAA_NCCL(c, n.GroupStart());
+  for (int q = 0; q < c->shard_world; ++q) {
+    int a = 0, b = 0;
+    shard_slices(d, q, c->shard_world, &a, &b);
+    if (b <= a) continue;
+    if (mode != edaa::kModeObj) {
+      double* pc = P<double>(c->part_C) + a * cblk;
+      EDAA_NCCL(c, n.Broadcast(pc, pc, (b - a) * cblk, ncclFloat64, q, c->comm, c->stream));
+    }
+    if (mode == edaa::kModeB || mode == edaa::kModeInit) {
+      double* pm = P<double>(c->part_m) + static_cast<size_t>(a) * d.Qs;
+      double* ps = P<double>(c->part_S) + static_cast<size_t>(a) * d.Qs;
+      EDAA_NCCL(c, n.Broadcast(pm, pm, static_cast<size_t>(b - a) * d.Qs, ncclFloat64, q, c->comm, c->stream));
+      EDAA_NCCL(c, n.Broadcast(ps, ps, static_cast<size_t>(b - a) * d.Qs, ncclFloat64, q, c->comm, c->stream));
+    } else {
+      double* po = P<double>(c->part_obj) + static_cast<size_t>(a) * d.M;
+      EDAA_NCCL(c, n.Broadcast(po, po, static_cast<size_t>(b - a) * d.M, ncclFloat64, q, c->comm, c->stream));
+    }
+  }
+  EDAA_NCCL(c, n.GroupEnd());
+  return EDAA_OK;
+}
+
+// Before the final phase: every rank's A and logits pixel columns to everyone,
+// and the per-run failure keys (set by the pass of the pixel's owner) min-reduced.
+int exchange_state(edaa_ctx* c) {
+  const Dims& d = c->d;
+  const NcclApi& n = nccl();
+  EDAA_NCCL(c, n.GroupStart());
+  EDAA_NCCL(c, n.AllReduce(c->fail_key.p, c->fail_key.p, d.M, ncclUint64, ncclMin, c->comm, c->stream));
+  for (int q = 0; q < c->shard_world; ++q) {
+    int a = 0, b = 0, j0 = 0, j1 = 0;
+    shard_slices(d, q, c->shard_world, &a, &b);
+    slice_pixels(d, a, b, &j0, &j1);
+    if (j1 <= j0) continue;
+    for (int row = 0; row < d.M * d.p; ++row) {
+      double* pa = P<double>(c->A) + static_cast<size_t>(row) * d.Npad + j0;
+      double* pl = P<double>(c->Lg) + static_cast<size_t>(row) * d.Npad + j0;
+      EDAA_NCCL(c, n.Broadcast(pa, pa, j1 - j0, ncclFloat64, q, c->comm, c->stream));
+      EDAA_NCCL(c, n.Broadcast(pl, pl, j1 - j0, ncclFloat64, q, c->comm, c->stream));
+    }
+  }
+  EDAA_NCCL(c, n.GroupEnd());
+  return EDAA_OK;
+}
+
+// One pass over the owned slices, then (sharded) the partial exchange.  In
+// emulation mode (development/tests, one device) the slice ranges of
+// shard_emulate ranks are launched one after another instead.
+int run_pass(edaa_ctx* c, int mode, edaa::PassArgs pa) {
+  if (c->shard_emulate > 1) {
+    for (int q = 0; q < c->shard_emulate; ++q) {
+      shard_slices(pa.d, q, c->shard_emulate, &pa.d.sl0, &pa.d.sl1);
+      if (pa.d.sl1 <= pa.d.sl0) continue;
+      const int rc = launch_pass_profiled(c, mode, pa);
+      if (rc) return rc;
+    }
+    return EDAA_OK;
+  }
+  const int rc = launch_pass_profiled(c, mode, pa);
+  if (rc || c->comm == nullptr) return rc;
+  return exchange_partials(c, mode);
 }
 
 int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
@@ -484,7 +643,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
   // ---- initialisation: B⁰, Y⁰ = X·B⁰, η, G ----
   {
     edaa::PassArgs pa = pass_args(c, 0, nullptr);
-    rc = launch_pass_profiled(c, edaa::kModeInit, pa);
+    rc = run_pass(c, edaa::kModeInit, pa);
     if (rc) return rc;
     EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, 0, edaa::kModeInit, 0), st), 2);
     EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostInit), st));
@@ -493,7 +652,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
     const int ti = static_cast<int>(t);
     edaa::PassArgs pa = pass_args(c, ti, P<double>(c->Y));
     if (hook) pa.observe_A = P<double>(c->obsA);
-    rc = launch_pass_profiled(c, edaa::kModeA, pa);
+    rc = run_pass(c, edaa::kModeA, pa);
     if (rc) return rc;
     EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeA, ti - 1), st), 2);
     if (hook) {
@@ -514,7 +673,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
     }
     for (size_t k = 1; k <= prm->inner_iters_b; ++k) {
       edaa::PassArgs pb = pass_args(c, ti, P<double>(c->Z));
-      rc = launch_pass_profiled(c, edaa::kModeB, pb);
+      rc = run_pass(c, edaa::kModeB, pb);
       if (rc) return rc;
       EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0), st), 2);
       if (k == prm->inner_iters_b) EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostG), st));
@@ -537,10 +696,14 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
   // ---- finalisation: trace[T], B̂, Ê = X·B̂, fit, coherence ----
   {
     edaa::PassArgs po = pass_args(c, static_cast<int>(c->T), P<double>(c->Y));
-    rc = launch_pass_profiled(c, edaa::kModeObj, po);
+    rc = run_pass(c, edaa::kModeObj, po);
     if (rc) return rc;
     edaa::CombineArgs co = combine_args(c, static_cast<int>(c->T), edaa::kModeObj, static_cast<int>(c->T));
     EDAA_LAUNCH(c, edaa::launch_combine(co, st));
+    if (c->comm) {
+      rc = exchange_state(c);
+      if (rc) return rc;
+    }
     EDAA_LAUNCH(c, edaa::launch_materialize_b(P<double>(c->Lg), P<double>(c->colm), P<double>(c->colS),
                                               P<double>(c->Bv), d, st));
     EDAA_LAUNCH(c, edaa::launch_strict_e(c->X, P<double>(c->Bv), P<double>(c->E), d, st));
@@ -599,6 +762,7 @@ int edaa_destroy(edaa_ctx* c) {
   if (c->X) cudaFree(c->X);
   if (c->xnorm) cudaFree(c->xnorm);
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->comm) nccl().CommDestroy(c->comm);
   cudaStreamDestroy(c->stream);
   delete c;
   return EDAA_OK;
@@ -775,6 +939,60 @@ int edaa_probe_fp64_peak(edaa_ctx* c, double* tflops) {
   cudaEventDestroy(e1);
   cudaFree(out);
   *tflops = best;
+  return EDAA_OK;
+}
+
+int edaa_nccl_unique_id(void* out, size_t bytes) {
+  if (!out || bytes < sizeof(ncclUniqueId)) return EDAA_ERR_INVALID;
+  const NcclApi& n = nccl();
+  if (!n.ok) return EDAA_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  if (n.GetUniqueId(&id) != ncclSuccess) return EDAA_ERR_CUDA;
+  std::memcpy(out, &id, sizeof id);
+  return EDAA_OK;
+}
+
+int edaa_set_pixel_shard(edaa_ctx* c, const void* id, size_t bytes, int rank, int world) {
+  if (!c) return EDAA_ERR_INVALID;
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (c->comm) {
+    nccl().CommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  c->shard_rank = 0;
+  c->shard_world = 1;
+  ++c->image_gen;  // captured schedules hold the old communicator
+  c->solved = false;
+  if (world <= 1 && id == nullptr) return EDAA_OK;  // sharding off
+  // (world == 1 with an id: a one-rank communicator — the exchange runs, as a check)
+  if (!id || bytes < sizeof(ncclUniqueId) || world < 1 || rank < 0 || rank >= world)
+    return set_err(c, EDAA_ERR_INVALID, "pixel shard: bad unique id, rank or world size");
+  const NcclApi& n = nccl();
+  if (!n.ok) return set_err(c, EDAA_ERR_UNSUPPORTED, "pixel shard: " + n.why);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  EDAA_NCCL(c, n.CommInitRank(&c->comm, world, uid, rank));
+  c->shard_rank = rank;
+  c->shard_world = world;
+  return EDAA_OK;
+}
+
+int edaa_set_shard_emulation(edaa_ctx* c, int world) {
+  if (!c || world < 0) return EDAA_ERR_INVALID;
+  if (c->comm) return set_err(c, EDAA_ERR_STATE, "shard emulation with a live communicator");
+  c->shard_emulate = world;
+  ++c->image_gen;
+  return EDAA_OK;
+}
+
+int edaa_shard_pixels(edaa_ctx* c, size_t* first, size_t* end) {
+  if (!c || !first || !end) return EDAA_ERR_INVALID;
+  if (!c->solved && c->d.nslices == 0) return set_err(c, EDAA_ERR_STATE, "no solve yet");
+  int j0 = 0, j1 = 0;
+  slice_pixels(c->d, c->d.sl0, c->d.sl1, &j0, &j1);
+  *first = static_cast<size_t>(std::min(j0, c->N));
+  *end = static_cast<size_t>(std::min(j1, c->N));
   return EDAA_OK;
 }
 

@@ -56,6 +56,7 @@ struct Dims {
   int nwb;    // W chunk buffers: 2 = next chunk prefetched, 1 = restaged in place
   int xbytes; // 4: fp32 image, 8: fp64 image (inputs not exactly representable in fp32)
   int ncta;   // persistent pass CTAs (one per SM)
+  int sl0, sl1;  // pixel slices this device owns (pixel sharding; 0..nslices otherwise)
 };
 
 struct PassArgs {

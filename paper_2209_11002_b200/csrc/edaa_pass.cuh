@@ -345,9 +345,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   const int nRT = (MODE == kModeA) ? nRTx + kQMax / 8 : nRTx;
   const int WST = w_stride(kQMax);
 
-  const int K = d.NCH * d.nslices;
-  const int item_begin = static_cast<int>((static_cast<long long>(blockIdx.x) * K) / gridDim.x);
-  const int item_end = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * K) / gridDim.x);
+  // the owned slices' items (all of them unless the pixels are sharded over devices)
+  const int K = d.NCH * (d.sl1 - d.sl0);
+  const int item_begin = d.sl0 * d.NCH + static_cast<int>((static_cast<long long>(blockIdx.x) * K) / gridDim.x);
+  const int item_end = d.sl0 * d.NCH + static_cast<int>((static_cast<long long>(blockIdx.x + 1) * K) / gridDim.x);
   int ntile = 0;
   for (int k = item_begin; k < item_end; ++k) {
     const int s = k / d.NCH;
@@ -768,7 +769,7 @@ enum PtSet : int { kPtAll = 0, kPtLo = 1, kPtHi = 2 };
 
 template <int MODE, int RTW, class XT, int PTS>
 cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
-  const dim3 grid(std::min(a.d.NCH * a.d.nslices, a.d.ncta));
+  const dim3 grid(std::min(a.d.NCH * (a.d.sl1 - a.d.sl0), a.d.ncta));
   const size_t smem = dev::smem_layout(a.d, a.d.nbuf).total;
   void (*kern)(PassArgs, CUtensorMap) = nullptr;
   if constexpr (MODE == kModeInit || MODE == kModeB) {

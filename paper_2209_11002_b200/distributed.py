@@ -139,3 +139,78 @@ def run_ensemble_sharded(x, config: edaa.EnsembleConfig, group=None,
     trace = v[o:o + T + 1].copy()
     rec = report.per_run[sel]
     return edaa.RunResult(E, A, B, rec.fit_l1, rec.coherence, rec.seed, rec.gamma, trace), report
+
+
+# ---------------------------------------------------------------------------
+# Pixel sharding of one solve: the pixels of a single run (or of a
+# whole batch) split over the ranks by pixel SLICE, the partial sums of every
+# pass exchanged over NCCL inside the device schedule (include/edaa_b200.h,
+# edaa_set_pixel_shard).  The host side here only distributes the communicator
+# id and mirrors the device's slice plan.
+
+NP = 32            # pixels per tile (csrc/edaa_internal.cuh kNP)
+TILES_PER_SLICE = 4
+MAX_SLICES = 148
+
+
+def pixel_slices(pixels: int) -> int:
+    """Number of pixel slices of an N-pixel image (a function of N only, as in make_dims)."""
+    ntiles = -(-pixels // NP)
+    return min(MAX_SLICES, -(-ntiles // TILES_PER_SLICE))
+
+
+def pixel_shard_plan(pixels: int, world: int, rank: int):
+    """(first slice, end slice, first pixel, end pixel) owned by `rank` — the
+    device's shard_slices / slice_pixels, clipped to the image."""
+    ntiles = -(-pixels // NP)
+    ns = pixel_slices(pixels)
+    if ns < world:
+        raise edaa.EdaaError("image too small to shard its pixels over that many devices")
+    s0, s1 = rank * ns // world, (rank + 1) * ns // world
+    j0, j1 = (s0 * ntiles // ns) * NP, (s1 * ntiles // ns) * NP
+    return s0, s1, min(j0, pixels), min(j1, pixels)
+
+
+def share_communicator_id(make_id: Callable[[], bytes], group=None) -> bytes:
+    """Rank 0 makes the NCCL id, every rank of `group` receives the same bytes."""
+    import torch.distributed as dist
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return obj[0]
+
+
+def join_pixel_shard(dev: "edaa.Device", group=None) -> int:
+    """Make `dev` this rank's member of a pixel-sharding communicator over `group`."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if world <= 1:
+        dev.set_pixel_shard(None, 0, 1)
+        return 1
+    uid = share_communicator_id(dev.nccl_unique_id, group)
+    dev.set_pixel_shard(uid, rank, world)
+    return world
+
+
+def run_pixel_sharded(x, config: edaa.SolverConfig, group=None, device: Optional[int] = None):
+    """Algorithm 1 for ONE run with its pixels split over the ranks of `group`
+    (one GPU each).  Every rank returns the full RunResult — bitwise the
+    single-GPU `edaa.run` result (the exchange keeps the fixed slice order)."""
+    import torch
+    config.validate()
+    xf = edaa.validate_image(x)
+    dev = edaa.Device.get(device if device is not None else torch.cuda.current_device())
+    join_pixel_shard(dev, group)
+    try:
+        dev.set_image(xf)
+        dev.solve(config.endmembers, config.outer_iters, config.inner_iters_a, config.inner_iters_b,
+                  [config.seed], [config.gamma])
+        rec = dev.record(0)
+        if not rec.ok:
+            raise edaa.EdaaError(rec.message.decode("utf-8"))
+        A, B, E = dev.factors(0)
+        return edaa.RunResult(E, A, B, rec.fit_l1, rec.coherence, config.seed, config.gamma,
+                              dev.traces()[0].copy())
+    finally:
+        dev.set_pixel_shard(None, 0, 1)

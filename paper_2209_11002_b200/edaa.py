@@ -269,6 +269,43 @@ class Device:
         self._check(self.lib.edaa_solve_observed(self.h, C.byref(prm), fn, None))
         del N
 
+    # -- pixel sharding (include/edaa_b200.h) -------------------------
+    @staticmethod
+    def _nccl_first():
+        # torch ships its own (newer) NCCL; it must be the copy the process binds
+        # libnccl.so.2 to, so load it before the library resolves NCCL lazily.
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
+
+    def nccl_unique_id(self) -> bytes:
+        """A fresh NCCL communicator id (rank 0 makes it, every rank joins with it)."""
+        self._nccl_first()
+        buf = C.create_string_buffer(128)
+        rc = self.lib.edaa_nccl_unique_id(buf, 128)
+        if rc != 0:
+            raise EdaaError("edaa_nccl_unique_id failed (rc=%d): NCCL unavailable" % rc, rc)
+        return buf.raw
+
+    def set_pixel_shard(self, uid: Optional[bytes], rank: int, world: int):
+        """Join the pixel-sharding communicator (collective over `world` ranks);
+        uid None turns sharding off (world 1 with a uid: one-rank self-check)."""
+        self._nccl_first()
+        buf = C.create_string_buffer(uid, 128) if uid else None
+        self._check(self.lib.edaa_set_pixel_shard(self.h, buf, 128 if uid else 0, int(rank), int(world)))
+
+    def shard_pixels(self):
+        """[first, end) pixel range this rank owned in the last solve."""
+        a, b = C.c_size_t(), C.c_size_t()
+        self._check(self.lib.edaa_shard_pixels(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def set_shard_emulation(self, world: int):
+        """Development/test: launch every pass as `world` slice-range launches on this one
+        device (the sharded decomposition without a collective); 0 or 1 turns it off."""
+        self._check(self.lib.edaa_set_shard_emulation(self.h, int(world)))
+
     # -- instrumentation ---------------------------------------------------------
     def profile_enable(self, on: bool = True):
         self._check(self.lib.edaa_profile_enable(self.h, int(on)))

@@ -74,3 +74,64 @@ def test_sharded_selection_matches_single_process(tmp_path, runs):
         assert np.array_equal(r["fits"], ref.fits)
         assert np.array_equal(r["A"], ref.A) and np.array_equal(r["B"], ref.B)
         assert np.array_equal(r["trace"], ref.trace)
+
+
+# ---- pixel sharding of one solve (distributed.run_pixel_sharded) -----------------
+
+@pytest.mark.parametrize("pixels", [1, 31, 500, 4000, 10000, 94249, 1048576])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_pixel_shard_plan_partitions_the_image(pixels, world):
+    ns = distributed.pixel_slices(pixels)
+    if ns < world:
+        with pytest.raises(edaa.EdaaError, match="too small"):
+            distributed.pixel_shard_plan(pixels, world, 0)
+        return
+    pix, sl = [], []
+    for r in range(world):
+        s0, s1, j0, j1 = distributed.pixel_shard_plan(pixels, world, r)
+        assert s1 > s0 and j0 % distributed.NP == 0
+        sl.append((s0, s1))
+        pix += list(range(j0, j1))
+    assert pix == list(range(pixels))                       # every pixel owned once, in order
+    assert sl[0][0] == 0 and sl[-1][1] == ns
+    assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))    # contiguous slice ranges
+
+
+class _FakeDevice:
+    """Records what the launcher asks of the device (the C-ABI needs a GPU)."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.calls = []
+
+    def nccl_unique_id(self):
+        return bytes([7, self.rank]) + bytes(126)
+
+    def set_pixel_shard(self, uid, rank, world):
+        self.calls.append((uid, rank, world))
+
+
+def _shard_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = _FakeDevice(rank)
+    w = distributed.join_pixel_shard(dev)
+    plan = distributed.pixel_shard_plan(10000, world, rank)
+    np.savez(out % rank, uid=np.frombuffer(dev.calls[0][0], np.uint8), rank=dev.calls[0][1],
+             world=dev.calls[0][2], w=w, plan=np.array(plan))
+    dist.destroy_process_group()
+
+
+def test_pixel_shard_join_shares_one_communicator_id(tmp_path):
+    """world 2 over gloo: rank 0's NCCL id reaches every rank unchanged, each joins
+    with its own rank, and the ranks' pixel plans tile the image."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "shard%d.npz")
+    mp.spawn(_shard_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    r0, r1 = np.load(out % 0), np.load(out % 1)
+    assert bytes(r0["uid"]) == bytes(r1["uid"]) == bytes([7, 0]) + bytes(126)
+    assert (int(r0["rank"]), int(r1["rank"])) == (0, 1)
+    assert int(r0["world"]) == int(r1["world"]) == 2 == int(r0["w"])
+    assert r0["plan"][3] == r1["plan"][2] and r0["plan"][2] == 0 and r1["plan"][3] == 10000
