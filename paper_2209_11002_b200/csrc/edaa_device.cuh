@@ -203,7 +203,9 @@ __device__ __forceinline__ void load_exp_table(double* T, int tid) {
 }
 
 __device__ __forceinline__ double exp_nonpos(double x, const double* T) {
-  if (!(x > -745.0)) return (x == x) ? 0.0 : x;  // −inf and underflow → 0; NaN stays NaN
+  // Branch-free: x ≤ −745 (incl. −inf) → 0, NaN → NaN by the final select; the
+  // 2^⌊k/256⌋ scale is split over two normal powers of two so denormal results
+  // (−745 < x < −708) round once, as std::exp's do.
   const double t = fma(x, 369.3299304675746, 6755399441055744.0);  // 256/ln2, 1.5·2^52
   const double kd = t - 6755399441055744.0;
   const int k = __double2loint(t);
@@ -214,11 +216,13 @@ __device__ __forceinline__ double exp_nonpos(double x, const double* T) {
   q = fma(q, r, 0.5);
   q = fma(q, r, 1.0);
   q = fma(q, r, 1.0);
-  const double y = q * T[k & (kExpTab - 1)];
   const int e = k >> 8;  // floor(k / 256)
-  if (e >= -1020) return __hiloint2double(__double2hiint(y) + (e << 20), __double2loint(y));
-  return ldexp(y, e);
+  const int e1 = e >> 1, e2 = e - e1;
+  const double ts = T[k & (kExpTab - 1)] * __hiloint2double((e1 + 1023) << 20, 0);  // off the chain
+  const double y = (q * ts) * __hiloint2double((e2 + 1023) << 20, 0);
+  return (x > -745.0) ? y : ((x == x) ? 0.0 : x);
 }
+
 
 // ---- mbarrier + TMA (cp.async.bulk.tensor) ----------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

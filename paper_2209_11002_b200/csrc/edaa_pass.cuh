@@ -145,7 +145,8 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     }
 #pragma unroll
     for (int o = 1; o < TPP; o <<= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-    const double inv = 1.0 / total;
+    // total ∈ [1e-30, p] (every factor ≤ 1, the largest ≥ 1e-30): a normal number.
+    const double inv = __drcp_rn(total);  // IEEE 1/total (= the division's value)
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       if (own[e]) {
@@ -514,17 +515,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     phase1(0, x_wait());
     cursor_next(p1c, d, slt);
     s_arrive(0);
-    for (int it = 0; it < ntile; ++it) {
-      // X(i+nbuf−1) into X(i−1)'s slot (released after P3(i−1)): nbuf−1 tiles of lead
-      if (it + nbuf - 1 < ntile) load_next_x(it + nbuf - 1);
+    // P1(i+1) overlaps the update of tile i (measured faster for both pass kinds than
+    // the serial order P3(i) → P1(i+1), EDAA_DBG=1024, which keeps the scalar fp64
+    // update chain clear of DMMA contention but leaves the tensor pipe idle meanwhile).
+    const bool serial = (pa.dbg & 1024) != 0;
+    auto next_p1 = [&](int it) {
       if (it + 1 < ntile) {
+        int xb;
         {
-          int xb;
-          {
-            EDAA_TSTART();
-            xb = x_wait();
-            EDAA_TSTOP(0);
-          }
+          EDAA_TSTART();
+          xb = x_wait();
+          EDAA_TSTOP(0);
+        }
+        {
           EDAA_TSTART();
           phase1(it + 1, xb);
           EDAA_TSTOP(1);
@@ -532,6 +535,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         cursor_next(p1c, d, slt);
         s_arrive(it + 1);
       }
+    };
+    for (int it = 0; it < ntile; ++it) {
+      // X(i+nbuf−1) into X(i−1)'s slot (released after P3(i−1)): nbuf−1 tiles of lead
+      if (it + nbuf - 1 < ntile) load_next_x(it + nbuf - 1);
+      if (!serial) next_p1(it);
       {
         EDAA_TSTART();
         w_wait(it);  // w(i), fac(i) ready
@@ -596,6 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       x_release();  // this warp is done with X(i) (P1(i) and P3(i))
       warp_arrive(sfree + (it & 1));  // … and with S(i)/w(i)
       cursor_next(p3c, d, slt);
+      if (serial) next_p1(it);
     }
   } else {
     // ========================== update group ==========================
