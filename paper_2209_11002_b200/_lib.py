@@ -88,10 +88,12 @@ _LIB = None
 
 
 def load(path: str = CUDA_LIB):
-    """Load libedaa_cuda.so (once). Raises EdaaError if it is not built."""
+    """Load libedaa_cuda.so (once). Raises EdaaError if it is not built.
+    EDAA_CUDA_LIB (development) names an alternative in-tree build of the same ABI."""
     global _LIB
     if _LIB is not None:
         return _LIB
+    path = os.environ.get("EDAA_CUDA_LIB", path)
     if not os.path.exists(path):
         raise EdaaError("libedaa_cuda.so is not built (run __graft_entry__.build()); "
                         "there is no CPU fallback")

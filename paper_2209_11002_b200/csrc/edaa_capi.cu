@@ -284,6 +284,7 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.Lrows = d.Lpad + d.QCpad;
   d.K1 = static_cast<int>(prm->inner_iters_a);
   d.ncta = c->num_sms;
+  d.pdl = (d.NCH * (d.sl1 - d.sl0) < c->num_sms) ? 1 : 0;
   // X ring depth and W chunk buffers, the deepest that fits shared memory.
   static const int kRing[][2] = {{4, 2}, {3, 2}, {3, 1}, {2, 2}, {2, 1}};
   for (const auto& rw : kRing) {
@@ -741,7 +742,7 @@ int edaa_create(int device, edaa_ctx** out) {
   if (const char* ng = std::getenv("EDAA_NO_GRAPH")) c->no_graph = ng[0] == '1';
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* kp = std::getenv("EDAA_KPROF"))
-    if (kp[0] == '1' && cudaMalloc(&c->kprof_buf, 24 * 8) == cudaSuccess) cudaMemset(c->kprof_buf, 0, 24 * 8);
+    if (kp[0] == '1' && cudaMalloc(&c->kprof_buf, 36 * 8) == cudaSuccess) cudaMemset(c->kprof_buf, 0, 36 * 8);
   *out = c;
   return EDAA_OK;
 }
@@ -882,13 +883,14 @@ int edaa_finish(edaa_ctx* c) {
   c->ev_used = 0;
   c->solved = true;
   if (c->kprof_buf) {
-    unsigned long long v[24];
+    unsigned long long v[36];
     cudaMemcpy(v, c->kprof_buf, sizeof v, cudaMemcpyDeviceToHost);
     const char* names[4] = {"init", "A", "B", "obj"};
     for (int m = 0; m < 4; ++m) {
       const unsigned long long* w = v + 6 * m;
-      std::fprintf(stderr, "[edaa kprof] %4s mma: x_wait %llu p1 %llu w_wait %llu p3 %llu | upd: s_wait %llu p2 %llu\n",
-                   names[m], w[0], w[1], w[2], w[3], w[4], w[5]);
+      std::fprintf(stderr, "[edaa kprof] %4s mma: x_wait %llu p1 %llu w_wait %llu p3 %llu | upd: s_wait %llu p2 %llu"
+                   " | cta: first-tile %llu loop-end sum %llu max %llu\n",
+                   names[m], w[0], w[1], w[2], w[3], w[4], w[5], v[24 + 3 * m], v[25 + 3 * m], v[26 + 3 * m]);
     }
     cudaMemset(c->kprof_buf, 0, sizeof v);
   }

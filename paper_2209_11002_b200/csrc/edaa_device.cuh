@@ -10,6 +10,15 @@ namespace dev {
 
 constexpr int kExpTab = 256;  // entries of the exp_nonpos table (2^(i/256))
 
+// Programmatic dependent launch: every kernel of the solve schedule is launched
+// with programmatic stream serialization (launch_pdl); it lets its successor
+// launch at once (launch_dependents at entry) and waits for its predecessor's
+// completion and memory (griddep_wait) before its first global read, so kernel
+// launch latency and per-CTA prologues overlap the previous kernel's tail.
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 __device__ __forceinline__ double log_floor() { return -69.07755278982137; }  // log(1e-30)
 
 // D = A·B + D for one 8×8×4 fp64 tile. Lane (g = lane>>2, t = lane&3) holds

@@ -17,6 +17,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace edaa {
@@ -57,6 +58,7 @@ struct Dims {
   int xbytes; // 4: fp32 image, 8: fp64 image (inputs not exactly representable in fp32)
   int ncta;   // persistent pass CTAs (one per SM)
   int sl0, sl1;  // pixel slices this device owns (pixel sharding; 0..nslices otherwise)
+  int pdl;       // programmatic dependent launch for the schedule's kernels (small grids only)
 };
 
 struct PassArgs {
@@ -122,6 +124,33 @@ struct PostArgs {
   int* fail_code;       // [M]
   double* fail_value;   // [M]
 };
+
+// Launch with programmatic stream serialization (see griddep_wait in edaa_device.cuh)
+// when `pdl`: the solve enables it only when the pass grid leaves SMs idle (small
+// images), where hiding launch latency pays; measured slower for full-grid passes
+// (cfg1: +2%), faster for cfg0 (-6%).  EDAA_NO_PDL=1 disables it everywhere.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("EDAA_NO_PDL");
+    return !(v && v[0] == '1');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // Kernel launchers (edaa_kernels.cu). All enqueue on `st`; none synchronise.
 cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st);

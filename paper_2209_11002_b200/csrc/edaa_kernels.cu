@@ -36,6 +36,8 @@ using namespace dev;
 
 // the slices, fixed xor-tree merge (deterministic).
 __global__ void k_colnorm(CombineArgs ca) {
+  griddep_launch_dependents();
+  griddep_wait();
   const Dims& d = ca.d;
   const int col = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -66,6 +68,8 @@ __global__ void k_colnorm(CombineArgs ca) {
 // Row sums over slices (fixed order): A mode → XAt / AAt; B/init → Y = Σ C_s·fac_s / S.
 // Block (32 columns × 8 rows); block (0,0) also folds the per-run objective.
 __global__ void k_rowsum(CombineArgs ca, int rows) {
+  griddep_launch_dependents();
+  griddep_wait();
   const Dims& d = ca.d;
   const int col = blockIdx.x * 32 + threadIdx.x;
   const int row = blockIdx.y * 8 + threadIdx.y;
@@ -110,6 +114,8 @@ constexpr int kCR = 2;
 constexpr int kCG = 4;
 
 __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ double red[kCR * kCG][kQMax];
   __shared__ double ys[kCR][kQMax];
   const Dims& d = ca.d;
@@ -172,6 +178,8 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
 // fixed xor tree — an order that depends on the slicing only.
 // grid = (NCH, ⌈RC·p²/8⌉ + 1): the last y-row of CTAs folds the traces.
 __global__ void __launch_bounds__(256) k_aat(CombineArgs ca) {
+  griddep_launch_dependents();
+  griddep_wait();
   const Dims& d = ca.d;
   const int S = d.nslices;
   const int p = d.p;
@@ -204,6 +212,8 @@ __global__ void __launch_bounds__(256) k_aat(CombineArgs ca) {
 // the bands, fixed xor tree).  The init Gram that feeds step_sizes keeps the
 // reference's band-ascending order in k_post.
 __global__ void __launch_bounds__(256) k_gram(PostArgs pa) {
+  griddep_launch_dependents();
+  griddep_wait();
   const Dims& d = pa.d;
   const int r = blockIdx.x;
   const int p = d.p;
@@ -223,6 +233,8 @@ __global__ void __launch_bounds__(256) k_gram(PostArgs pa) {
 // ---------------------------------------------------------------------------
 // Per-run small algebra: Z = XAᵀ − Y·AAᵀ, G = YᵀY, and (init) the step sizes.
 __global__ void __launch_bounds__(256) k_post(PostArgs pa) {
+  griddep_launch_dependents();
+  griddep_wait();
   const Dims& d = pa.d;
   const int r = blockIdx.x;
   const int p = d.p;
@@ -494,24 +506,25 @@ cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st) {
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   const Dims& d = a.d;
   if (a.mode == kModeObj) {  // the final objective only
-    k_rowsum<<<dim3((d.Qs + 31) / 32, 1), dim3(32, 8), 0, st>>>(a, 0);
+    cudaError_t e0 = launch_pdl(d.pdl != 0, k_rowsum, dim3((d.Qs + 31) / 32, 1), dim3(32, 8), 0, st, a, 0);
+    if (e0 != cudaSuccess) return e0;
     return cudaGetLastError();
   }
   if (a.mode == kModeA)
-    k_aat<<<dim3(d.NCH, (d.RC * d.p * d.p + 7) / 8 + 1), 256, 0, st>>>(a);
+    launch_pdl(d.pdl != 0, k_aat, dim3(d.NCH, (d.RC * d.p * d.p + 7) / 8 + 1), dim3(256), 0, st, a);
   else
-    k_colnorm<<<(d.Qs + 7) / 8, 256, 0, st>>>(a);
+    launch_pdl(d.pdl != 0, k_colnorm, dim3((d.Qs + 7) / 8), dim3(256), 0, st, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_combine<<<dim3(d.NCH, (d.Lpad + kCR - 1) / kCR), 256, 0, st>>>(a);
+  launch_pdl(d.pdl != 0, k_combine, dim3(d.NCH, (d.Lpad + kCR - 1) / kCR), dim3(256), 0, st, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_post(const PostArgs& a, cudaStream_t st) {
   if (a.mode == kPostG)
-    k_gram<<<a.d.M, 256, 0, st>>>(a);
+    launch_pdl(a.d.pdl != 0, k_gram, dim3(a.d.M), dim3(256), 0, st, a);
   else
-    k_post<<<a.d.M, 256, 0, st>>>(a);
+    launch_pdl(a.d.pdl != 0, k_post, dim3(a.d.M), dim3(256), 0, st, a);
   return cudaGetLastError();
 }
 

@@ -31,10 +31,15 @@
 
 #include "edaa_device.cuh"
 
+#ifndef EDAA_P1_UNROLL
+#define EDAA_P1_UNROLL 2
+#endif
+
 namespace edaa {
 namespace pass_impl {
 
 using namespace dev;
+constexpr int kP1Unroll = EDAA_P1_UNROLL;  // P1 band-pair loop unroll (dev sweeps via -D)
 
 inline int pt_bucket(int p) {
   if (p <= 8) return p;
@@ -316,6 +321,7 @@ __device__ __forceinline__ ChunkInfo chunk_info(const Dims& d, int chunk) {
 template <int MODE, int PT, int RTW, class XT>
 __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const long long t_kernel0 = pa.kprof ? clock64() : 0;
   const Dims& d = pa.d;
   const int nbuf = d.nbuf;
   const SmemLayout lay = smem_layout(d, nbuf);
@@ -388,6 +394,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   auto w_wait = [&](int i) { mbar_wait(wready + (i & 1), (i >> 1) & 1); };
   if (tid < kQMax) facb[tid] = facb[kQMax + tid] = 1.0;
   load_exp_table(etab, tid);
+  griddep_launch_dependents();
+  griddep_wait();  // the previous kernel's W / partial normalisers / state are complete
   __syncthreads();
 
   if (mma_group) {
@@ -490,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       const int h0 = 2 * (d.Lpad / 16);
       const int mb = (half ? h0 : 0) / 2;
       const int mn = (half ? d.Lpad / 4 - h0 : h0) / 2;
-#pragma unroll 2
+#pragma unroll kP1Unroll
       for (int m2 = 0; m2 < mn; ++m2) {
         const int m = mb + m2;
         const XT* xr = xs + m * 8 * kXRow<XT>;
@@ -513,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     if (MODE != kModeInit && !(pa.dbg & 65)) w_fetch(item_chunk(item_begin), 0);  // the first chunk (waited in P1(0))
     for (int f = 0; f < nbuf - 1 && f < ntile; ++f) load_next_x(f);  // X(0 .. nbuf−2) in flight
     phase1(0, x_wait());
+    if (pa.kprof && gtid == 0) atomicAdd(pa.kprof + 24 + 3 * MODE, static_cast<unsigned long long>(clock64() - t_kernel0));
     cursor_next(p1c, d, slt);
     s_arrive(0);
     // P1(i+1) overlaps the update of tile i (measured faster for both pass kinds than
@@ -605,6 +614,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       warp_arrive(sfree + (it & 1));  // … and with S(i)/w(i)
       cursor_next(p3c, d, slt);
       if (serial) next_p1(it);
+    }
+    if (pa.kprof && gtid == 0) {  // per-CTA MMA-loop end: sum and max over CTAs
+      const unsigned long long tt = static_cast<unsigned long long>(clock64() - t_kernel0);
+      atomicAdd(pa.kprof + 25 + 3 * MODE, tt);
+      atomicMax(pa.kprof + 26 + 3 * MODE, tt);
     }
   } else {
     // ========================== update group ==========================
@@ -800,7 +814,8 @@ cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads, smem, st>>>(a, *static_cast<const CUtensorMap*>(a.xmap));
+  e = launch_pdl(a.d.pdl != 0, kern, grid, dim3(kThreads), smem, st, a, *static_cast<const CUtensorMap*>(a.xmap));
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
