@@ -742,7 +742,7 @@ int edaa_create(int device, edaa_ctx** out) {
   if (const char* ng = std::getenv("EDAA_NO_GRAPH")) c->no_graph = ng[0] == '1';
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* kp = std::getenv("EDAA_KPROF"))
-    if (kp[0] == '1' && cudaMalloc(&c->kprof_buf, 36 * 8) == cudaSuccess) cudaMemset(c->kprof_buf, 0, 36 * 8);
+    if (kp[0] == '1' && cudaMalloc(&c->kprof_buf, 52 * 8) == cudaSuccess) cudaMemset(c->kprof_buf, 0, 52 * 8);
   *out = c;
   return EDAA_OK;
 }
@@ -883,14 +883,15 @@ int edaa_finish(edaa_ctx* c) {
   c->ev_used = 0;
   c->solved = true;
   if (c->kprof_buf) {
-    unsigned long long v[36];
+    unsigned long long v[52];
     cudaMemcpy(v, c->kprof_buf, sizeof v, cudaMemcpyDeviceToHost);
     const char* names[4] = {"init", "A", "B", "obj"};
     for (int m = 0; m < 4; ++m) {
       const unsigned long long* w = v + 6 * m;
       std::fprintf(stderr, "[edaa kprof] %4s mma: x_wait %llu p1 %llu w_wait %llu p3 %llu | upd: s_wait %llu p2 %llu"
-                   " | cta: first-tile %llu loop-end sum %llu max %llu\n",
-                   names[m], w[0], w[1], w[2], w[3], w[4], w[5], v[24 + 3 * m], v[25 + 3 * m], v[26 + 3 * m]);
+                   " | cta: setup %llu x0 %llu w0 %llu first-tile %llu loop-end sum %llu max %llu\n",
+                   names[m], w[0], w[1], w[2], w[3], w[4], w[5], v[36 + 4 * m], v[37 + 4 * m], v[38 + 4 * m],
+                   v[24 + 3 * m], v[25 + 3 * m], v[26 + 3 * m]);
     }
     cudaMemset(c->kprof_buf, 0, sizeof v);
   }

@@ -140,7 +140,9 @@ __host__ __device__ inline SmemLayout smem_layout(const Dims& d, int nbuf) {
 // to the exponent field with an integer add.  10 fp64-pipe instructions on the
 // dependent chain, against ~20 for libdevice exp: these scalar fp64 ops share the
 // pipe with the DMMA contractions and sit on the per-pixel update's critical path.
-__constant__ double kExp2Tab[kExpTab] = {
+// In global memory, not __constant__: every thread loads a different entry, which the
+// constant cache would serialise (measured ~4k cycles of pass-kernel prologue).
+__device__ const double kExp2Tab[kExpTab] = {
     1.0, 1.0027112750502025, 1.0054299011128027, 1.0081558981184175,
     1.0108892860517005, 1.0136300849514894, 1.016378314910953, 1.019133996077738,
     1.0218971486541166, 1.0246677928971357, 1.0274459491187637, 1.030231637686041,

@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   griddep_launch_dependents();
   griddep_wait();  // the previous kernel's W / partial normalisers / state are complete
   __syncthreads();
+  if (pa.kprof && tid == 0) atomicAdd(pa.kprof + 36 + 4 * MODE, static_cast<unsigned long long>(clock64() - t_kernel0));
 
   if (mma_group) {
     // =========================== MMA group ===========================
@@ -469,6 +470,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         if (d.nwb == 2) {
           if (wchunk >= 0) wcur ^= 1;
           cp_async_wait0();
+          if (pa.kprof && gtid == 0 && wchunk < 0)
+            atomicAdd(pa.kprof + 38 + 4 * MODE, static_cast<unsigned long long>(clock64() - t_kernel0));
           bar_sync(bars::kMma, kGroup);
           if (p1c.item + 1 < item_end && item_chunk(p1c.item + 1) != chunk)
             w_fetch(item_chunk(p1c.item + 1), wcur ^ 1);
@@ -520,7 +523,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
 
     if (MODE != kModeInit && !(pa.dbg & 65)) w_fetch(item_chunk(item_begin), 0);  // the first chunk (waited in P1(0))
     for (int f = 0; f < nbuf - 1 && f < ntile; ++f) load_next_x(f);  // X(0 .. nbuf−2) in flight
-    phase1(0, x_wait());
+    {
+      const int xb0 = x_wait();
+      if (pa.kprof && gtid == 0) atomicAdd(pa.kprof + 37 + 4 * MODE, static_cast<unsigned long long>(clock64() - t_kernel0));
+      phase1(0, xb0);
+    }
     if (pa.kprof && gtid == 0) atomicAdd(pa.kprof + 24 + 3 * MODE, static_cast<unsigned long long>(clock64() - t_kernel0));
     cursor_next(p1c, d, slt);
     s_arrive(0);
