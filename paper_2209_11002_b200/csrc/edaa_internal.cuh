@@ -20,6 +20,10 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 
+#ifndef EDAA_QMAX
+#define EDAA_QMAX 24
+#endif
+
 namespace edaa {
 
 constexpr int kThreads = 512;   // 16 warps per CTA: 8 MMA warps + 8 update warps
@@ -27,7 +31,7 @@ constexpr int kGroup = 256;     // threads per warp group
 constexpr int kNP = 32;         // pixels per tile
 constexpr int kXST = kNP + 8;   // fp32 X tile row stride (conflict-free DMMA B-frags)
 constexpr int kSST = kNP + 4;   // fp64 weight tile row stride
-constexpr int kQMax = 24;       // columns per chunk (3 DMMA column tiles)
+constexpr int kQMax = EDAA_QMAX;  // columns per chunk (kQMax/8 DMMA column tiles)
 constexpr int kMaxCT = kQMax / 8;
 constexpr int kMaxSlices = 148; // bounds the slice-partial traffic (nslices·(L+24)·Q doubles per pass)
 constexpr int kTilesPerSlice = 4;  // 128-pixel slices: ~5 (slice, chunk) items per CTA at cfg1
