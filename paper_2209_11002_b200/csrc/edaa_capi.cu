@@ -646,7 +646,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
     edaa::PassArgs pa = pass_args(c, 0, nullptr);
     rc = run_pass(c, edaa::kModeInit, pa);
     if (rc) return rc;
-    EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, 0, edaa::kModeInit, 0), st), 2);
+    EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, 0, edaa::kModeInit, 0), st));
     EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostInit), st));
   }
   for (size_t t = 1; t <= c->T; ++t) {
@@ -676,7 +676,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
       edaa::PassArgs pb = pass_args(c, ti, P<double>(c->Z));
       rc = run_pass(c, edaa::kModeB, pb);
       if (rc) return rc;
-      EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0), st), 2);
+      EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0), st));
       if (k == prm->inner_iters_b) EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostG), st));
       if (hook) {
         rc = download_b(c, hook);

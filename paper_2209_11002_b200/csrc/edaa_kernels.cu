@@ -172,6 +172,129 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
   }
 }
 
+// B step / init combine in ONE kernel: column normalisers, Y rows and Z rows.
+// CTA = (run chunk, kBR band rows), 256 threads.  Every CTA of a chunk first
+// recomputes that chunk's 24 column normalisers (the few-KB part_m/part_S
+// columns; identical arithmetic in every CTA), keeps e^{m_s−m} in shared memory, then sums its rows'
+// slice partials in kCG contiguous groups added in order (k_combine's order),
+// and forms Z = XAᵀ − Y·AAᵀ.  One launch instead of two, and the rescale
+// factors come from shared memory instead of a global scratch array.
+constexpr int kBR = 8;
+
+__global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
+  griddep_launch_dependents();
+  griddep_wait();
+  extern __shared__ __align__(16) double facs[];  // [nslices][kQMax]
+  __shared__ double cS[kQMax];
+  __shared__ double red[kCG][kBR][kQMax];
+  __shared__ double ys[kBR][kQMax];
+  const Dims& d = ca.d;
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x;
+  const int col0 = chunk * d.QCpad;
+  const int S = d.nslices;
+  const int ncol = min(d.RC, d.M - chunk * d.RC) * d.p;
+  // Normalisers: 8 threads per column (192 threads for the 24 columns); thread t
+  // of a column takes slices t, t+8, … with all its loads issued up front, then
+  // an xor tree over the 8 (fixed order: a function of the slicing only).
+  if (tid < kQMax * 8) {
+    const int cc = tid >> 3, t8 = tid & 7;
+    const int col = col0 + cc;
+    constexpr int kPer = (kMaxSlices + 7) / 8;
+    double mv[kPer], sv[kPer];
+    double m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int sl = t8 + 8 * k;
+      mv[k] = (sl < S) ? ca.part_m[static_cast<size_t>(sl) * d.Qs + col] : -INFINITY;
+      sv[k] = (sl < S) ? ca.part_S[static_cast<size_t>(sl) * d.Qs + col] : 0.0;
+      m = fmax(m, mv[k]);
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double Ssum = 0.0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int sl = t8 + 8 * k;
+      if (sl < S) {
+        const double f = (mv[k] == -INFINITY) ? 0.0 : exp(mv[k] - m);
+        facs[sl * kQMax + cc] = f;
+        Ssum += sv[k] * f;
+      }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) Ssum += __shfl_xor_sync(0xffffffffu, Ssum, o);
+    if (t8 == 0) {
+      cS[cc] = Ssum;
+      if (blockIdx.y == 0) {
+        ca.colm[col] = m;
+        ca.colS[col] = Ssum;
+        ca.collogS[col] = log(Ssum);
+        const int r = chunk * d.RC + cc / d.p;
+        if (cc < d.RC * d.p && r < d.M && !(isfinite(m) && isfinite(Ssum) && Ssum > 0.0))
+          atomicMin(ca.fail_key + r, (static_cast<unsigned long long>(ca.t) << 1) | 1ull);
+      }
+    }
+  }
+  __syncthreads();
+  const int l0 = blockIdx.y * kBR;
+  const int nr = min(kBR, d.Lpad - l0);
+  const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
+  // kCG·kBR·kQMax = 768 (group, row, column) sums over 256 threads: each thread
+  // runs its three with interleaved loads (all of a group's slices in flight).
+  {
+    constexpr int kIt = kCG * kBR * kQMax / 256;
+    const double* src[kIt];
+    double v[kIt];
+    int s0[kIt], len[kIt], xs[kIt], slot[kIt];
+    int maxlen = 0;
+#pragma unroll
+    for (int q = 0; q < kIt; ++q) {
+      const int e = tid + 256 * q;
+      const int x = e % kQMax, rest = e / kQMax;
+      const int rr = rest % kBR, g = rest / kBR;
+      s0[q] = (g * S) / kCG;
+      len[q] = (rr < nr) ? ((g + 1) * S) / kCG - s0[q] : 0;
+      src[q] = ca.part_C + static_cast<size_t>(l0 + min(rr, nr - 1)) * d.Qs + col0 + x;
+      xs[q] = x;
+      slot[q] = (g * kBR + rr) * kQMax + x;
+      v[q] = 0.0;
+      maxlen = max(maxlen, len[q]);
+    }
+#pragma unroll 5
+    for (int k = 0; k < maxlen; ++k) {
+#pragma unroll
+      for (int q = 0; q < kIt; ++q)
+        if (k < len[q]) {
+          const int sl = s0[q] + k;
+          v[q] += src[q][sl * sstride] * facs[sl * kQMax + xs[q]];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kIt; ++q) (&red[0][0][0])[slot[q]] = v[q];
+  }  __syncthreads();
+  for (int e = tid; e < nr * kQMax; e += blockDim.x) {
+    const int x = e % kQMax, rr = e / kQMax;
+    double v = red[0][rr][x];
+    for (int k = 1; k < kCG; ++k) v += red[k][rr][x];
+    v = (x < ncol) ? v / cS[x] : 0.0;  // padding columns carry no run
+    ca.Y[static_cast<size_t>(l0 + rr) * d.Qs + col0 + x] = v;
+    ys[rr][x] = v;
+  }
+  if (ca.Z == nullptr) return;
+  __syncthreads();
+  for (int e = tid; e < nr * kQMax; e += blockDim.x) {
+    const int x = e % kQMax, rr = e / kQMax;
+    if (x >= ncol) continue;
+    const int rl = x / d.p;
+    const double* arow = ca.AAt + static_cast<size_t>(rl * d.p) * d.Qs + col0 + x;  // AAᵀ[rl·p+m][x]
+    double sacc = 0.0;
+    for (int mm = 0; mm < d.p; ++mm) sacc += ys[rr][rl * d.p + mm] * arow[static_cast<size_t>(mm) * d.Qs];
+    const size_t o = static_cast<size_t>(l0 + rr) * d.Qs + col0 + x;
+    ca.Z[o] = ca.XAt[o] - sacc;
+  }
+}
+
 // A block: the run-diagonal AAᵀ blocks (pseudo-band rows Lpad + rl·p + i of the
 // slice partials) and the objective trace.  One warp per output: lane k sums
 // the contiguous slice range [k·S/32, (k+1)·S/32) in ascending order, then a
@@ -510,10 +633,18 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
     if (e0 != cudaSuccess) return e0;
     return cudaGetLastError();
   }
-  if (a.mode == kModeA)
-    launch_pdl(d.pdl != 0, k_aat, dim3(d.NCH, (d.RC * d.p * d.p + 7) / 8 + 1), dim3(256), 0, st, a);
-  else
-    launch_pdl(d.pdl != 0, k_colnorm, dim3((d.Qs + 7) / 8), dim3(256), 0, st, a);
+  if (a.mode != kModeA) {  // B step / init: normalisers, Y and Z in one kernel
+    static bool attr = false;
+    if (!attr) {
+      const cudaError_t ea = cudaFuncSetAttribute(k_combine_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kMaxSlices * kQMax * static_cast<int>(sizeof(double)));
+      if (ea != cudaSuccess) return ea;
+      attr = true;
+    }
+    return launch_pdl(d.pdl != 0, k_combine_b, dim3(d.NCH, (d.Lpad + kBR - 1) / kBR), dim3(256),
+                      static_cast<size_t>(d.nslices) * kQMax * sizeof(double), st, a);
+  }
+  launch_pdl(d.pdl != 0, k_aat, dim3(d.NCH, (d.RC * d.p * d.p + 7) / 8 + 1), dim3(256), 0, st, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   launch_pdl(d.pdl != 0, k_combine, dim3(d.NCH, (d.Lpad + kCR - 1) / kCR), dim3(256), 0, st, a);
