@@ -100,6 +100,20 @@ EDAA_API int edaa_set_image_host(edaa_ctx* ctx, const float* x, size_t bands, si
 EDAA_API int edaa_set_image_host_f64(edaa_ctx* ctx, const double* x, size_t bands, size_t pixels);
 EDAA_API int edaa_set_image_device(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels, size_t ld);
 
+/* Ingest on the device: HsiImage::validate + l2_normalize
+ * (image.cpp:10-47) fused into the upload.  x: the RAW L×N image (fp64,
+ * row-major).  Errors carry the reference's messages ("image: non-finite
+ * reflectance" / "image: negative reflectance" for the first offending element
+ * in scan order, "degenerate input: all pixels are zero"); zero pixels are
+ * listed ascending (the first zero_cap of them; *n_zero = their count) and left
+ * unnormalised, as NormalizeResult::zero_pixels.  The normalised values are
+ * bitwise the reference's; when all are exactly representable in fp32 the
+ * solve uses the fp32 image, else the fp64 one.  edaa_image_get returns the
+ * context's image as L×N fp64 (and its storage width, 4 or 8 bytes). */
+EDAA_API int edaa_ingest_host(edaa_ctx* ctx, const double* x, size_t bands, size_t pixels,
+                              size_t* zero_pixels, size_t zero_cap, size_t* n_zero);
+EDAA_API int edaa_image_get(edaa_ctx* ctx, double* out, int* xbytes);
+
 /* Batched Algorithm 1 over all runs.  _async only enqueues on edaa_stream();
  * edaa_finish waits and fetches the per-run records.  edaa_solve = both. */
 EDAA_API int edaa_solve_async(edaa_ctx* ctx, const edaa_solve_params* params);

@@ -246,6 +246,37 @@ static int check_iterate(const double* m, size_t d, size_t cols, size_t outer, c
   return 0;
 }
 
+/* ---- ingest: image.cpp:10-47 ------------------------------------------------ */
+int orc_l2_normalize(const double* x, size_t l, size_t n, double* out, size_t* zero, size_t* n_zero,
+                     char* err, size_t errlen) {
+  /* HsiImage::validate: the first offending value in row-major order decides */
+  if (l < 1 || n < 1) return fail(err, errlen, "image: needs at least one band and one pixel");
+  for (size_t k = 0; k < l * n; ++k) {
+    if (!isfinite(x[k])) return fail(err, errlen, "image: non-finite reflectance");
+    if (x[k] < 0.0) return fail(err, errlen, "image: negative reflectance");
+  }
+  size_t nz = 0;
+  int any = 0;
+  for (size_t j = 0; j < n; ++j) {
+    double s = 0.0; /* Matrix::column_norm, matrix.cpp:44-51 */
+    for (size_t i = 0; i < l; ++i) {
+      const double v = x[i * n + j];
+      s += v * v;
+    }
+    const double norm = sqrt(s);
+    if (norm == 0.0) {
+      zero[nz++] = j;
+      for (size_t i = 0; i < l; ++i) out[i * n + j] = x[i * n + j];
+      continue;
+    }
+    any = 1;
+    for (size_t i = 0; i < l; ++i) out[i * n + j] = x[i * n + j] / norm;
+  }
+  *n_zero = nz;
+  if (!any) return fail(err, errlen, "degenerate input: all pixels are zero");
+  return 0;
+}
+
 /* ---- Algorithm 1: solver.cpp:190-238 -------------------------------------- */
 int orc_run(const double* x, size_t l, size_t n, size_t p, size_t t_outer, size_t k1, size_t k2,
             double gamma, uint64_t seed, double* trace, double* a_out, double* b_out,

@@ -25,6 +25,10 @@
 extern "C" {
 #endif
 
+/* HsiImage::validate + l2_normalize, image.cpp:10-47 (zero pixels listed, left as is) */
+int orc_l2_normalize(const double* x, size_t l, size_t n, double* out, size_t* zero, size_t* n_zero,
+                     char* err, size_t errlen);
+
 /* SplitMix64, prng.hpp:15-26 */
 uint64_t orc_splitmix_next(uint64_t* state);
 double orc_splitmix_unit(uint64_t* state);

@@ -77,6 +77,19 @@ class Oracle:
         if rc != 0:
             raise OracleError(self._err.value.decode("utf-8"))
 
+    # -- ingest -----------------------------------------------------------------
+    def l2_normalize(self, x):
+        """(normalised L×N, zero pixels) — image.cpp:29-47 (validation included)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        L, N = x.shape
+        out = np.zeros((L, N))
+        zero = np.zeros(max(N, 1), dtype=np.uint64)
+        nz = _sz()
+        f = self._f("l2_normalize")
+        f.argtypes = [_dp, _sz, _sz, _dp, _u64p, C.POINTER(_sz), C.c_char_p, _sz]
+        self._check(f(x, L, N, out, zero, C.byref(nz), self._err, 512))
+        return out, [int(v) for v in zero[:nz.value]]
+
     # -- solver -----------------------------------------------------------------
     def run(self, x, p, T=100, K1=5, K2=5, gamma=1.0, seed=0) -> RunOut:
         x = np.ascontiguousarray(x, dtype=np.float64)

@@ -61,6 +61,22 @@ void copy_result(const ar::RunResult& r, double* trace, double* a, double* b, do
 
 extern "C" {
 
+// l2_normalize (image.cpp:29-47), validation included. out: L×N; zero: up to n entries.
+int oref_l2_normalize(const double* x, size_t l, size_t n, double* out, size_t* zero, size_t* n_zero,
+                      char* err, size_t errlen) {
+  try {
+    ar::HsiImage img = make_image(x, l, n);
+    const ar::NormalizeResult r = ar::l2_normalize(img);
+    copy_out(r.image.data, out);
+    *n_zero = r.zero_pixels.size();
+    std::copy(r.zero_pixels.begin(), r.zero_pixels.end(), zero);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(e, err, errlen);
+    return 1;
+  }
+}
+
 int oref_prng_u64(uint64_t seed, size_t count, uint64_t* out) {
   ar::Prng rng(seed);
   for (size_t i = 0; i < count; ++i) out[i] = rng.next_u64();

@@ -53,6 +53,9 @@ SIGNATURES = [
     ("edaa_set_image_host_f64", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t]),
     ("edaa_set_image_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
                                         C.c_size_t]),
+    ("edaa_ingest_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p,
+                                   C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("edaa_image_get", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]),
     ("edaa_solve_async", C.c_int, [C.c_void_p, C.POINTER(SolveParams)]),
     ("edaa_finish", C.c_int, [C.c_void_p]),
     ("edaa_solve", C.c_int, [C.c_void_p, C.POINTER(SolveParams)]),

@@ -55,7 +55,8 @@ struct edaa_ctx {
   };
   Buf A, Lg, Bv, Y, Z, XAt, AAt, Gbuf, colm, colS, collogS, eta_a, eta_b, gamma, trace, part_C,
       part_m, part_S, part_obj, fac, E, fit, mu, part_fit, seeds, fail_key, fail_code, fail_value, cand,
-      selected, fit_min, obsA, pr_b, pr_a, pr_y, pr_r, pr_g, pr_rat, pr_part, pr_out;
+      selected, fit_min, obsA, pr_b, pr_a, pr_y, pr_r, pr_g, pr_rat, pr_part, pr_out, in_raw, in_x,
+      in_flags, in_bad;
   int fit_blocks = 0;
   // instrumentation
   bool profile = false;
@@ -138,6 +139,51 @@ __global__ void k_pad_copy(const XT* src, size_t ld, XT* dst, int L, int N, int 
     const int l = static_cast<int>(i / Npad), j = static_cast<int>(i % Npad);
     dst[i] = (j < N) ? src[static_cast<size_t>(l) * ld + j] : XT(0);
   }
+}
+
+// Device ingest (HsiImage::validate + l2_normalize, image.cpp:10-47): one thread
+// per pixel.  Validation records the first offending element in the
+// reference's scan order (row-major, i·N + j) per kind; the norm is
+// Matrix::column_norm (matrix.cpp:44-51: s += v·v band-ascending, no fused
+// multiply-add, sqrt) and every element of a nonzero pixel is divided by it, so
+// the result is bitwise the reference's.  Zero pixels are flagged and left as
+// they are; `inexact` is raised if any normalised value is not representable in
+// fp32 (then the solve keeps the fp64 image).
+__global__ void k_ingest(const double* raw, double* xn, int L, int N, int Npad, unsigned long long* bad,
+                         unsigned char* zero, unsigned int* inexact) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Npad) return;
+  if (j >= N) {
+    for (int i = 0; i < L; ++i) xn[static_cast<size_t>(i) * Npad + j] = 0.0;
+    return;
+  }
+  double s = 0.0;
+  for (int i = 0; i < L; ++i) {
+    const double v = raw[static_cast<size_t>(i) * N + j];
+    const unsigned long long idx = static_cast<unsigned long long>(i) * N + j;
+    if (!isfinite(v))
+      atomicMin(bad + 0, idx);
+    else if (v < 0.0)
+      atomicMin(bad + 1, idx);
+    s = __dadd_rn(s, __dmul_rn(v, v));
+  }
+  const double norm = sqrt(s);
+  const bool z = (norm == 0.0);
+  zero[j] = z ? 1 : 0;
+  bool exact = true;
+  for (int i = 0; i < L; ++i) {
+    const double v = raw[static_cast<size_t>(i) * N + j];
+    const double o = z ? v : __ddiv_rn(v, norm);
+    xn[static_cast<size_t>(i) * Npad + j] = o;
+    exact &= (static_cast<double>(static_cast<float>(o)) == o);
+  }
+  if (!exact) atomicOr(inexact, 1u);
+}
+
+__global__ void k_to_f32(const double* src, float* dst, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<float>(src[i]);
 }
 
 // Register-resident DMMA loop: 4 independent accumulators per lane.
@@ -757,7 +803,7 @@ int edaa_destroy(edaa_ctx* c) {
                            &c->fit, &c->mu, &c->part_fit, &c->seeds, &c->fail_key, &c->fail_code,
                            &c->fail_value, &c->cand, &c->selected, &c->fit_min, &c->obsA,
                            &c->pr_b, &c->pr_a, &c->pr_y, &c->pr_r, &c->pr_g, &c->pr_rat,
-                           &c->pr_part, &c->pr_out};
+                           &c->pr_part, &c->pr_out, &c->in_raw, &c->in_x, &c->in_flags, &c->in_bad};
   for (auto* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->X) cudaFree(c->X);
@@ -843,6 +889,82 @@ int edaa_set_image_device(edaa_ctx* c, const float* x, size_t bands, size_t pixe
   d.Npad = c->Npad;
   d.xbytes = 4;
   EDAA_LAUNCH(c, edaa::launch_xnorm(c->X, c->xnorm, d, c->stream));
+  return EDAA_OK;
+}
+
+int edaa_ingest_host(edaa_ctx* c, const double* x, size_t bands, size_t pixels, size_t* zero_pixels,
+                     size_t zero_cap, size_t* n_zero) {
+  if (!c || !x) return set_err(c, EDAA_ERR_INVALID, "null argument");
+  if (bands < 1 || pixels < 1) return set_err(c, EDAA_ERR_INVALID, "image: needs at least one band and one pixel");
+  if (pixels > (1u << 30) || bands > (1u << 20)) return set_err(c, EDAA_ERR_UNSUPPORTED, "image too large");
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  const int L = static_cast<int>(bands), N = static_cast<int>(pixels);
+  const int Npad = (N + edaa::kNP - 1) / edaa::kNP * edaa::kNP;
+  const size_t raw_bytes = bands * pixels * 8, xn_bytes = static_cast<size_t>(L) * Npad * 8;
+  EDAA_CUDA(c, ensure(c->in_raw, raw_bytes));
+  EDAA_CUDA(c, ensure(c->in_x, xn_bytes));
+  EDAA_CUDA(c, ensure(c->in_flags, static_cast<size_t>(Npad)));
+  EDAA_CUDA(c, ensure(c->in_bad, 24));
+  cudaStream_t st = c->stream;
+  EDAA_CUDA(c, cudaMemcpyAsync(c->in_raw.p, x, raw_bytes, cudaMemcpyHostToDevice, st));
+  EDAA_CUDA(c, cudaMemsetAsync(c->in_bad.p, 0xFF, 16, st));
+  EDAA_CUDA(c, cudaMemsetAsync(static_cast<char*>(c->in_bad.p) + 16, 0, 8, st));
+  unsigned long long* bad = P<unsigned long long>(c->in_bad);
+  k_ingest<<<(Npad + 127) / 128, 128, 0, st>>>(P<double>(c->in_raw), P<double>(c->in_x), L, N, Npad, bad,
+                                               P<unsigned char>(c->in_flags),
+                                               reinterpret_cast<unsigned int*>(bad + 2));
+  EDAA_LAUNCH(c, cudaGetLastError());
+  unsigned long long hb[3];
+  std::vector<unsigned char> flags(N);
+  EDAA_CUDA(c, cudaMemcpyAsync(hb, bad, 24, cudaMemcpyDeviceToHost, st));
+  EDAA_CUDA(c, cudaMemcpyAsync(flags.data(), c->in_flags.p, N, cudaMemcpyDeviceToHost, st));
+  EDAA_CUDA(c, cudaStreamSynchronize(st));
+  if (hb[0] != ~0ull || hb[1] != ~0ull)  // the reference throws at the first offending element
+    return set_err(c, EDAA_ERR_INVALID, hb[0] < hb[1] ? "image: non-finite reflectance" : "image: negative reflectance");
+  size_t nz = 0;
+  for (int j = 0; j < N; ++j)
+    if (flags[j]) {
+      if (zero_pixels && nz < zero_cap) zero_pixels[nz] = static_cast<size_t>(j);
+      ++nz;
+    }
+  if (n_zero) *n_zero = nz;
+  if (nz == pixels) return set_err(c, EDAA_ERR_INVALID, "degenerate input: all pixels are zero");
+  const int xbytes = (static_cast<unsigned int>(hb[2]) == 0u) ? 4 : 8;  // fp32-exact → the fp32 image path
+  int rc = prepare_image(c, bands, pixels, xbytes);
+  if (rc) return rc;
+  if (xbytes == 4) {
+    k_to_f32<<<592, 256, 0, st>>>(P<double>(c->in_x), static_cast<float*>(c->X), static_cast<size_t>(L) * Npad);
+    EDAA_LAUNCH(c, cudaGetLastError());
+  } else {
+    EDAA_CUDA(c, cudaMemcpyAsync(c->X, c->in_x.p, xn_bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  Dims d{};
+  d.L = c->L;
+  d.N = c->N;
+  d.Npad = c->Npad;
+  d.xbytes = xbytes;
+  EDAA_LAUNCH(c, edaa::launch_xnorm(c->X, c->xnorm, d, st));
+  return EDAA_OK;
+}
+
+int edaa_image_get(edaa_ctx* c, double* out, int* xbytes) {
+  if (!c || !out) return EDAA_ERR_INVALID;
+  if (!c->X) return set_err(c, EDAA_ERR_STATE, "no image set");
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  const size_t n = static_cast<size_t>(c->L) * c->Npad;
+  std::vector<double> buf(n);
+  if (c->xbytes == 8) {
+    EDAA_CUDA(c, cudaMemcpyAsync(buf.data(), c->X, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    std::vector<float> f(n);
+    EDAA_CUDA(c, cudaMemcpyAsync(f.data(), c->X, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < n; ++i) buf[i] = f[i];
+  }
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (int l = 0; l < c->L; ++l)
+    std::memcpy(out + static_cast<size_t>(l) * c->N, buf.data() + static_cast<size_t>(l) * c->Npad, c->N * 8);
+  if (xbytes) *xbytes = c->xbytes;
   return EDAA_OK;
 }
 

@@ -161,10 +161,15 @@ def validate_image(x) -> np.ndarray:
     arr = np.asarray(x)
     if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
         raise EdaaError("image: needs at least one band and one pixel")
-    if not np.all(np.isfinite(arr)):
-        raise EdaaError("image: non-finite reflectance")
-    if np.any(arr < 0):
-        raise EdaaError("image: negative reflectance")
+    # the reference throws at the first offending element in row-major order
+    flat = arr.ravel()
+    nonfin = np.flatnonzero(~np.isfinite(flat))
+    neg = np.flatnonzero(np.isfinite(flat) & (flat < 0))
+    if nonfin.size or neg.size:
+        first_nonfin = nonfin[0] if nonfin.size else flat.size
+        first_neg = neg[0] if neg.size else flat.size
+        raise EdaaError("image: non-finite reflectance" if first_nonfin < first_neg
+                        else "image: negative reflectance")
     if arr.dtype == np.float32:
         return np.ascontiguousarray(arr)
     a64 = np.ascontiguousarray(arr, dtype=np.float64)
@@ -233,6 +238,27 @@ class Device:
         fn = self.lib.edaa_set_image_host_f64 if xf.dtype == np.float64 else self.lib.edaa_set_image_host
         self._check(fn(self.h, xf.ctypes.data_as(C.c_void_p), xf.shape[0], xf.shape[1]))
         self.L, self.N = xf.shape
+
+    def ingest(self, x) -> List[int]:
+        """Validate + ℓ2-normalise a RAW L×N image on the device (image.cpp:10-47);
+        it becomes this device's image.  Returns the zero pixels (left as they are)."""
+        xr = np.ascontiguousarray(x, dtype=np.float64)
+        if xr.ndim != 2:
+            raise EdaaError("image: needs at least one band and one pixel")
+        L, N = xr.shape
+        zp = np.zeros(max(N, 1), dtype=np.uint64)
+        nz = C.c_size_t()
+        self._check(self.lib.edaa_ingest_host(self.h, xr.ctypes.data_as(C.c_void_p), L, N,
+                                              zp.ctypes.data_as(C.c_void_p), zp.size, C.byref(nz)))
+        self.L, self.N = L, N
+        return [int(v) for v in zp[:nz.value]]
+
+    def image(self):
+        """(the device image as L×N fp64, its storage width in bytes: 4 or 8)."""
+        out = np.zeros((self.L, self.N))
+        xb = C.c_int()
+        self._check(self.lib.edaa_image_get(self.h, out.ctypes.data_as(C.c_void_p), C.byref(xb)))
+        return out, xb.value
 
     # -- solve ------------------------------------------------------------------
     def _params(self, p, T, K1, K2, seeds, gammas):
@@ -397,6 +423,16 @@ def run(x, config: SolverConfig, observer: Optional[Callable] = None, device: in
     if not rec.ok:
         raise EdaaError(rec.message.decode("utf-8"))
     return _result(dev, 0, config.seed, config.gamma, dev.traces())
+
+
+def l2_normalize(x, device: int = 0):
+    """l2_normalize (image.cpp:29-47) on the GPU, validation included; returns
+    (normalised L×N fp64 image, zero pixels).  The image stays resident on the
+    device for a following solve."""
+    dev = Device.get(device)
+    zero = dev.ingest(x)
+    img, _ = dev.image()
+    return img, zero
 
 
 def ensemble_plan(config: EnsembleConfig, first: int = 0, count: Optional[int] = None):

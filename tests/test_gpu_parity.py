@@ -317,3 +317,47 @@ def test_pixel_sharded_run_through_torch_distributed_world1():
         assert np.array_equal(got.objective_trace, ref.objective_trace)
     finally:
         dist.destroy_process_group()
+
+
+# ---- ingest on the device (validate + l2_normalize fused into the upload, §8f rank 2) ----
+
+def test_device_ingest_is_bitwise_the_reference_l2_normalize():
+    from oracle import Oracle
+    rng = np.random.default_rng(3)
+    x = rng.random((37, 1000)) ** 2
+    x[:, [5, 640, 999]] = 0.0
+    got, zero = edaa.l2_normalize(x)
+    want, wzero = Oracle().l2_normalize(x)
+    assert zero == wzero == [5, 640, 999]
+    assert np.array_equal(got, want)
+    assert dev().image()[1] == 8  # not fp32-exact: the fp64 image path
+
+
+def test_device_ingest_errors_and_fp32_detection():
+    x = np.ones((4, 9))
+    y = x.copy(); y[1, 2] = -1.0; y[3, 0] = np.nan
+    with pytest.raises(edaa.EdaaError, match="negative reflectance"):
+        dev().ingest(y)
+    y = x.copy(); y[1, 2] = np.inf; y[3, 0] = -2.0
+    with pytest.raises(edaa.EdaaError, match="non-finite reflectance"):
+        dev().ingest(y)
+    with pytest.raises(edaa.EdaaError, match="degenerate input: all pixels are zero"):
+        dev().ingest(np.zeros((3, 5)))
+    onehot = np.zeros((6, 64))
+    onehot[np.arange(64) % 6, np.arange(64)] = 2.5
+    assert dev().ingest(onehot) == []
+    img, xbytes = dev().image()
+    assert xbytes == 4 and np.array_equal(img, onehot / 2.5)
+
+
+def test_solve_after_device_ingest_equals_solve_on_host_normalised_image():
+    from oracle import Oracle
+    raw = synth.small_scene(30, 2000, 3, seed=6).astype(np.float64) * 3.7
+    d = dev()
+    zero = d.ingest(raw)
+    assert zero == []
+    d.solve(3, 8, 5, 5, [1], [2.0])
+    A1, B1, E1 = d.factors(0)
+    norm, _ = Oracle().l2_normalize(raw)
+    r = edaa.run(norm, edaa.SolverConfig(endmembers=3, outer_iters=8, gamma=2.0, seed=1))
+    assert np.array_equal(A1, r.abundances) and np.array_equal(B1, r.contributions)

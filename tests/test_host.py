@@ -163,3 +163,15 @@ def test_coherence_matches_oracle(oracle_kinds):  # ensemble.cpp:41-60, test_ens
         e = rng.random((int(rng.integers(1, 40)), int(rng.integers(2, 9))))
         for norm in (False, True):
             assert edaa.coherence(e, norm) == orc.coherence(e, norm)
+
+
+def test_validate_image_reports_first_offending_element():
+    """edaa.validate_image follows HsiImage::validate's scan order (image.cpp:10-27)."""
+    from paper_2209_11002_b200 import edaa
+    x = np.ones((3, 5))
+    y = x.copy(); y[0, 4] = -1.0; y[2, 0] = np.nan
+    with pytest.raises(edaa.EdaaError, match="negative reflectance"):
+        edaa.validate_image(y)
+    y = x.copy(); y[0, 4] = np.nan; y[2, 0] = -1.0
+    with pytest.raises(edaa.EdaaError, match="non-finite reflectance"):
+        edaa.validate_image(y)

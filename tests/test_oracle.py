@@ -168,3 +168,36 @@ def test_port_reproduces_golden(name):
         e = orc.run_ensemble(x, int(g["p"]), M=int(g["M"]), T=int(g["T"]))
         assert np.array_equal(e.fits, g["fits"]) and e.selected == int(g["selected"])
         assert e.candidates == [int(c) for c in g["candidates"]]
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_l2_normalize_restatement_matches_reference(seed):
+    """image.cpp:29-47 restated in oracle/edaa_oracle.c: bitwise the reference,
+    zero pixels listed and left as they are."""
+    from oracle import Oracle
+    if "reference" not in available_kinds():
+        pytest.skip("reference oracle not built")
+    rng = np.random.default_rng(seed)
+    x = rng.random((13, 300)) ** 3
+    x[:, [0, 77, 299]] = 0.0
+    a, za = Oracle("reference").l2_normalize(x)
+    b, zb = Oracle("port").l2_normalize(x)
+    assert np.array_equal(a, b) and za == zb == [0, 77, 299]
+    assert np.array_equal(a[:, 77], x[:, 77])
+
+
+@pytest.mark.parametrize("kind", ["reference", "port"])
+def test_l2_normalize_error_messages_follow_scan_order(kind):
+    """HsiImage::validate throws at the first offending element (row-major)."""
+    from oracle import Oracle, OracleError
+    if kind not in available_kinds():
+        pytest.skip("oracle not built")
+    x = np.ones((4, 9))
+    y = x.copy(); y[1, 2] = -1.0; y[3, 0] = np.nan
+    with pytest.raises(OracleError, match="negative reflectance"):
+        Oracle(kind).l2_normalize(y)
+    y = x.copy(); y[1, 2] = np.inf; y[3, 0] = -2.0
+    with pytest.raises(OracleError, match="non-finite reflectance"):
+        Oracle(kind).l2_normalize(y)
+    with pytest.raises(OracleError, match="degenerate input: all pixels are zero"):
+        Oracle(kind).l2_normalize(np.zeros((3, 5)))
