@@ -225,10 +225,7 @@ constexpr int kXRow = 128 / sizeof(XT);
 template <int R, bool PSEUDO, int RTW, class XT>
 __device__ __forceinline__ void accumulate_tiles(double (&ac)[RTW][kMaxCT][2], const XT* xs,
                                                  const double* w, int gwarp, int nRTx, int g, int t4,
-                                                 int xrows) {
-  int xo[kNP / 4];
-#pragma unroll
-  for (int kk = 0; kk < kNP / 4; ++kk) xo[kk] = xoff<XT>(g, kk * 4 + t4, xrows);
+                                                 const int (&xo)[kNP / 4]) {
   const double* wrow = w + g * kSST + t4;
   const double* prow = w + ((gwarp + 8 * R - nRTx) * 8 + g) * kSST + t4;  // the pseudo tile's rows
 #pragma unroll
@@ -431,6 +428,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     auto item_chunk = [&](int item) { return item - (item / d.NCH) * d.NCH; };
 
     const int xrows = x_rows(d), brows = x_box_rows(d);
+    // Per-lane constants of the DMMA fragment addressing, hoisted out of the tile loop:
+    // P3's swizzled X offsets per k-step and P1's two band-pair offsets / band range.
+    int xo3[kNP / 4];
+#pragma unroll
+    for (int kk = 0; kk < kNP / 4; ++kk) xo3[kk] = xoff<XT>(g, kk * 4 + t4, xrows);
+    const int p1_pt = gwarp & 3, p1_half = gwarp >> 2;
+    const int p1_xo0 = xoff<XT>(2 * t4, p1_pt * 8 + g, xrows), p1_xo1 = xoff<XT>(2 * t4 + 1, p1_pt * 8 + g, xrows);
+    const int p1_h0 = 2 * (d.Lpad / 16);
+    const int p1_mb = (p1_half ? p1_h0 : 0) / 2;
+    const int p1_mn = (p1_half ? d.Lpad / 4 - p1_h0 : p1_h0) / 2;
     const int nbox = xrows / brows, nhalf = sizeof(XT) / 4;  // row boxes × column halves
     const unsigned tile_tx = static_cast<unsigned>(nbox * nhalf * brows * 128);
     // Producer (MMA thread 0): X(f) into slot f % nbuf once the slot's previous
@@ -489,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       }
       const double* ws = ws_buf(wcur);
       const XT* xs = xslot(xb);
-      const int pt = gwarp & 3, half = gwarp >> 2;
+      const int pt = p1_pt, half = p1_half;
       double c1[kMaxCT][2];
 #pragma unroll
       for (int c = 0; c < kMaxCT; ++c) c1[c][0] = c1[c][1] = 0.0;
@@ -498,11 +505,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       // both the X B-fragment (rows 2·t4+par hit distinct 128-byte swizzle chunks)
       // and the W A-fragment (row stride 2·WST words ≡ 8 mod 32) conflict-free.
       const double* wcol = ws + 2 * t4 * WST + g;
-      const int xo0 = xoff<XT>(2 * t4, pt * 8 + g, xrows), xo1 = xoff<XT>(2 * t4 + 1, pt * 8 + g, xrows);
+      const int xo0 = p1_xo0, xo1 = p1_xo1;
       // band halves of even k-step length: K4 = Lpad/4 is even, split at h0 = 2⌊K4/4⌋
-      const int h0 = 2 * (d.Lpad / 16);
-      const int mb = (half ? h0 : 0) / 2;
-      const int mn = (half ? d.Lpad / 4 - h0 : h0) / 2;
+      const int mb = p1_mb, mn = p1_mn;
 #pragma unroll kP1Unroll
       for (int m2 = 0; m2 < mn; ++m2) {
         const int m = mb + m2;
@@ -584,18 +589,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         EDAA_TSTART();
         if (!(pa.dbg & 129)) {
           switch (my_x + (my_pseudo ? 8 : 0)) {  // warp-uniform: the DMMAs below are unpredicated
-            case 1: accumulate_tiles<1, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 2: accumulate_tiles<2, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 3: accumulate_tiles<3, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 4: if constexpr (RTW >= 4) accumulate_tiles<4, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 5: if constexpr (RTW >= 5) accumulate_tiles<5, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 6: if constexpr (RTW >= 6) accumulate_tiles<6, false>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 8: if constexpr (MODE == kModeA) accumulate_tiles<0, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 9: if constexpr (MODE == kModeA) accumulate_tiles<1, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 10: if constexpr (MODE == kModeA) accumulate_tiles<2, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 11: if constexpr (MODE == kModeA) accumulate_tiles<3, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 12: if constexpr (MODE == kModeA && RTW >= 5) accumulate_tiles<4, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
-            case 13: if constexpr (MODE == kModeA && RTW >= 6) accumulate_tiles<5, true>(acc, xs, w, gwarp, nRTx, g, t4, xrows); break;
+            case 1: accumulate_tiles<1, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 2: accumulate_tiles<2, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 3: accumulate_tiles<3, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 4: if constexpr (RTW >= 4) accumulate_tiles<4, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 5: if constexpr (RTW >= 5) accumulate_tiles<5, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 6: if constexpr (RTW >= 6) accumulate_tiles<6, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 8: if constexpr (MODE == kModeA) accumulate_tiles<0, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 9: if constexpr (MODE == kModeA) accumulate_tiles<1, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 10: if constexpr (MODE == kModeA) accumulate_tiles<2, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 11: if constexpr (MODE == kModeA) accumulate_tiles<3, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 12: if constexpr (MODE == kModeA && RTW >= 5) accumulate_tiles<4, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 13: if constexpr (MODE == kModeA && RTW >= 6) accumulate_tiles<5, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
             default: break;
           }
         }
