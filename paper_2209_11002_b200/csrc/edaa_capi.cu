@@ -788,7 +788,7 @@ int edaa_create(int device, edaa_ctx** out) {
   if (const char* ng = std::getenv("EDAA_NO_GRAPH")) c->no_graph = ng[0] == '1';
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* kp = std::getenv("EDAA_KPROF"))
-    if (kp[0] == '1' && cudaMalloc(&c->kprof_buf, 52 * 8) == cudaSuccess) cudaMemset(c->kprof_buf, 0, 52 * 8);
+    if (kp[0] == '1' && cudaMalloc(&c->kprof_buf, 64 * 8) == cudaSuccess) cudaMemset(c->kprof_buf, 0, 64 * 8);
   *out = c;
   return EDAA_OK;
 }
@@ -828,9 +828,12 @@ static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels, int xbytes) {
   c->N = static_cast<int>(pixels);
   c->Npad = (c->N + edaa::kNP - 1) / edaa::kNP * edaa::kNP;
   c->xbytes = xbytes;
-  ++c->image_gen;  // X contents change: tensor map and graph are rebuilt
+  // A captured solve schedule reads X and ‖x‖² through their device addresses and
+  // the shape through Dims (part of the graph key), so new contents in the same
+  // buffers replay the same graph; only a reallocation invalidates it.
   const size_t xb = static_cast<size_t>(c->L) * c->Npad * xbytes;
   if (c->x_cap < xb) {
+    ++c->image_gen;
     if (c->X) cudaFree(c->X);
     c->X = nullptr;
     c->x_cap = 0;
@@ -839,6 +842,7 @@ static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels, int xbytes) {
   }
   const size_t nb = static_cast<size_t>(c->Npad) * 8;
   if (c->xn_cap < nb) {
+    ++c->image_gen;
     if (c->xnorm) cudaFree(c->xnorm);
     c->xnorm = nullptr;
     c->xn_cap = 0;
@@ -1005,15 +1009,15 @@ int edaa_finish(edaa_ctx* c) {
   c->ev_used = 0;
   c->solved = true;
   if (c->kprof_buf) {
-    unsigned long long v[52];
+    unsigned long long v[64];
     cudaMemcpy(v, c->kprof_buf, sizeof v, cudaMemcpyDeviceToHost);
     const char* names[4] = {"init", "A", "B", "obj"};
     for (int m = 0; m < 4; ++m) {
       const unsigned long long* w = v + 6 * m;
       std::fprintf(stderr, "[edaa kprof] %4s mma: x_wait %llu p1 %llu w_wait %llu p3 %llu | upd: s_wait %llu p2 %llu"
-                   " | cta: setup %llu x0 %llu w0 %llu first-tile %llu loop-end sum %llu max %llu\n",
+                   " | cta: setup %llu x0 %llu w0 %llu first-tile %llu loop-end sum %llu max %llu | ldx %llu rel %llu\n",
                    names[m], w[0], w[1], w[2], w[3], w[4], w[5], v[36 + 4 * m], v[37 + 4 * m], v[38 + 4 * m],
-                   v[24 + 3 * m], v[25 + 3 * m], v[26 + 3 * m]);
+                   v[24 + 3 * m], v[25 + 3 * m], v[26 + 3 * m], v[52 + 2 * m], v[53 + 2 * m]);
     }
     cudaMemset(c->kprof_buf, 0, sizeof v);
   }

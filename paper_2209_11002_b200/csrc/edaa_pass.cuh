@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       if (i >= kNSB) mbar_wait(sfree + (i & 1), ((i >> 1) - 1) & 1);  // w(i−2) consumed
       if (MODE == kModeInit || (pa.dbg & 65)) return;
       const int chunk = p1c.chunk;
-      if (chunk != wchunk) {
+      if (chunk != wchunk && !(pa.dbg & 4096)) {
         // Switch to the prefetched buffer once every MMA warp is past its previous
         // P1 (so the old buffer is free), then prefetch the following item's chunk.
         if (d.nwb == 2) {
@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         }
         wchunk = chunk;
       }
+      if (pa.dbg & 2048) return;
       const double* ws = ws_buf(wcur);
       const XT* xs = xslot(xb);
       const int pt = p1_pt, half = p1_half;
@@ -561,7 +562,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     };
     for (int it = 0; it < ntile; ++it) {
       // X(i+nbuf−1) into X(i−1)'s slot (released after P3(i−1)): nbuf−1 tiles of lead
-      if (it + nbuf - 1 < ntile) load_next_x(it + nbuf - 1);
+      {
+        const long long tq_ = (pa.kprof && lane == 0 && gwarp == 0) ? clock64() : 0;
+        if (it + nbuf - 1 < ntile) load_next_x(it + nbuf - 1);
+        if (pa.kprof && lane == 0 && gwarp == 0)
+          atomicAdd(pa.kprof + 52 + 2 * MODE, static_cast<unsigned long long>(clock64() - tq_));
+      }
       if (!serial) next_p1(it);
       {
         EDAA_TSTART();
@@ -624,9 +630,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           }
         }
       }
+      const long long tr_ = (pa.kprof && lane == 0 && gwarp == 0) ? clock64() : 0;
       x_release();  // this warp is done with X(i) (P1(i) and P3(i))
       warp_arrive(sfree + (it & 1));  // … and with S(i)/w(i)
       cursor_next(p3c, d, slt);
+      if (pa.kprof && lane == 0 && gwarp == 0)
+        atomicAdd(pa.kprof + 53 + 2 * MODE, static_cast<unsigned long long>(clock64() - tr_));
       if (serial) next_p1(it);
     }
     if (pa.kprof && gtid == 0) {  // per-CTA MMA-loop end: sum and max over CTAs

@@ -161,6 +161,15 @@ def validate_image(x) -> np.ndarray:
     arr = np.asarray(x)
     if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
         raise EdaaError("image: needs at least one band and one pixel")
+    # fast path: min/max reductions (NaN propagates through min) settle a clean image
+    if arr.dtype.kind == "f" and arr.size:
+        lo, hi = arr.min(), arr.max()
+        if lo >= 0 and np.isfinite(hi):
+            if arr.dtype == np.float32:
+                return np.ascontiguousarray(arr)
+            a64 = np.ascontiguousarray(arr, dtype=np.float64)
+            a32 = a64.astype(np.float32)
+            return a32 if np.array_equal(a32.astype(np.float64), a64) else a64
     # the reference throws at the first offending element in row-major order
     flat = arr.ravel()
     nonfin = np.flatnonzero(~np.isfinite(flat))
