@@ -197,12 +197,18 @@ __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
   // Normalisers: 8 threads per column (192 threads for the 24 columns); thread t
   // of a column takes slices t, t+8, … with all its loads issued up front, then
   // an xor tree over the 8 (fixed order: a function of the slicing only).
-  if (tid < kQMax * 8) {
-    const int cc = tid >> 3, t8 = tid & 7;
-    const int col = col0 + cc;
-    constexpr int kPer = (kMaxSlices + 7) / 8;
-    double mv[kPer], sv[kPer];
-    double m = -INFINITY;
+  // The exponentials are exp_nonpos (table + polynomial, ~1 ulp; every argument
+  // m_s − m ≤ 0): its table load is in flight with the partial loads, and it is
+  // about half the fp64 work of libdevice exp on this latency-bound prologue.
+  __shared__ double etab[kExpTab];
+  const double tabv = (tid < kExpTab) ? kExp2Tab[tid] : 0.0;
+  const bool nact = tid < kQMax * 8;
+  const int cc = tid >> 3, t8 = tid & 7;
+  const int col = col0 + cc;
+  constexpr int kPer = (kMaxSlices + 7) / 8;
+  double mv[kPer], sv[kPer];
+  double m = -INFINITY;
+  if (nact) {
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const int sl = t8 + 8 * k;
@@ -212,12 +218,16 @@ __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
     }
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  if (tid < kExpTab) etab[tid] = tabv;
+  __syncthreads();
+  if (nact) {
     double Ssum = 0.0;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const int sl = t8 + 8 * k;
       if (sl < S) {
-        const double f = (mv[k] == -INFINITY) ? 0.0 : exp(mv[k] - m);
+        const double f = (mv[k] == -INFINITY) ? 0.0 : exp_nonpos(mv[k] - m, etab);
         facs[sl * kQMax + cc] = f;
         Ssum += sv[k] * f;
       }
