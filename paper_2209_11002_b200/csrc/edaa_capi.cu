@@ -331,6 +331,10 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.K1 = static_cast<int>(prm->inner_iters_a);
   d.ncta = c->num_sms;
   d.pdl = (d.NCH * (d.sl1 - d.sl0) < c->num_sms) ? 1 : 0;
+  // Chunk-major pass items when X is comfortably L2-resident (126 MB L2 on B200,
+  // shared with the slice partials); EDAA_SLICE_MAJOR=1 forces slice-major.
+  static const bool slice_major = std::getenv("EDAA_SLICE_MAJOR") != nullptr;
+  d.cmajor = (!slice_major && static_cast<size_t>(d.Lpad) * d.Npad * d.xbytes <= (size_t(96) << 20)) ? 1 : 0;
   // X ring depth and W chunk buffers, the deepest that fits shared memory.
   static const int kRing[][2] = {{4, 2}, {3, 2}, {3, 1}, {2, 2}, {2, 1}};
   for (const auto& rw : kRing) {

@@ -275,17 +275,36 @@ __host__ __device__ __forceinline__ int slice_tile(const Dims& d, int s) {
   return (s * d.ntiles) / d.nslices;  // < 2^31: ntiles ≤ 2^25, nslices ≤ 296
 }
 // slt: the CTA's shared-memory copy of slice_tile(d, 0 .. nslices) (no divisions per tile)
+// Item order (local index k over the owned slices [sl0, sl1)):
+//   chunk-major (Dims::cmajor): k = chunk·nsl + (slice − sl0) — a CTA's block of
+//     items is consecutive slices of one run chunk, so the W chunk and the per-
+//     column constants change about once per CTA instead of once per item; X is
+//     re-read from L2 once per chunk (chosen when X fits in L2);
+//   slice-major: k = (slice − sl0)·NCH + chunk — consecutive items re-read the
+//     same X slice (large images).
+// Either order computes the same per-(slice, chunk) partials: results are bitwise equal.
+__host__ __device__ __forceinline__ int item_slice(const Dims& d, int k) {
+  return d.cmajor ? d.sl0 + k % (d.sl1 - d.sl0) : d.sl0 + k / d.NCH;
+}
+__host__ __device__ __forceinline__ int item_chunk(const Dims& d, int k) {
+  return d.cmajor ? k / (d.sl1 - d.sl0) : k % d.NCH;
+}
 __device__ __forceinline__ void cursor_set(Cursor& c, const Dims& d, const int* slt, int item) {
   c.item = item;
-  c.slice = item / d.NCH;
-  c.chunk = item - c.slice * d.NCH;
+  c.slice = item_slice(d, item);
+  c.chunk = item_chunk(d, item);
   c.tile = c.tstart = slt[c.slice];
   c.tend = slt[c.slice + 1];
 }
 __device__ __forceinline__ void cursor_next(Cursor& c, const Dims& d, const int* slt) {
   if (++c.tile != c.tend) return;
-  ++c.item;  // slice-major: the next chunk of the same slice, then the next slice
-  if (++c.chunk == d.NCH) {
+  ++c.item;
+  if (d.cmajor) {  // the next slice of the same chunk, then the next chunk
+    if (++c.slice == d.sl1) {
+      c.slice = d.sl0;
+      ++c.chunk;
+    }
+  } else if (++c.chunk == d.NCH) {  // the next chunk of the same slice, then the next slice
     c.chunk = 0;
     ++c.slice;
   }
@@ -353,11 +372,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
 
   // the owned slices' items (all of them unless the pixels are sharded over devices)
   const int K = d.NCH * (d.sl1 - d.sl0);
-  const int item_begin = d.sl0 * d.NCH + static_cast<int>((static_cast<long long>(blockIdx.x) * K) / gridDim.x);
-  const int item_end = d.sl0 * d.NCH + static_cast<int>((static_cast<long long>(blockIdx.x + 1) * K) / gridDim.x);
+  const int item_begin = static_cast<int>((static_cast<long long>(blockIdx.x) * K) / gridDim.x);
+  const int item_end = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * K) / gridDim.x);
   int ntile = 0;
   for (int k = item_begin; k < item_end; ++k) {
-    const int s = k / d.NCH;
+    const int s = item_slice(d, k);
     ntile += slice_tile(d, s + 1) - slice_tile(d, s);
   }  // once per CTA
   if (ntile == 0) return;
@@ -425,7 +444,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       }
       cp_async_commit();
     };
-    auto item_chunk = [&](int item) { return item - (item / d.NCH) * d.NCH; };
 
     const int xrows = x_rows(d), brows = x_box_rows(d);
     // Per-lane constants of the DMMA fragment addressing, hoisted out of the tile loop:
@@ -482,8 +500,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           if (pa.kprof && gtid == 0 && wchunk < 0)
             atomicAdd(pa.kprof + 38 + 4 * MODE, static_cast<unsigned long long>(clock64() - t_kernel0));
           bar_sync(bars::kMma, kGroup);
-          if (p1c.item + 1 < item_end && item_chunk(p1c.item + 1) != chunk)
-            w_fetch(item_chunk(p1c.item + 1), wcur ^ 1);
+          // the next item with a different chunk (chunk-major: usually none in this CTA)
+          int nx = p1c.item + 1;
+          if (d.cmajor) nx = (item_chunk(d, nx) == chunk) ? (chunk + 1) * (d.sl1 - d.sl0) : nx;
+          if (nx < item_end && item_chunk(d, nx) != chunk) w_fetch(item_chunk(d, nx), wcur ^ 1);
         } else {  // one buffer: restage in place once every MMA warp is past its previous P1
           if (wchunk >= 0) {
             bar_sync(bars::kMma, kGroup);
@@ -529,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
             make_double2(c1[ct][0], c1[ct][1]);
     };
 
-    if (MODE != kModeInit && !(pa.dbg & 65)) w_fetch(item_chunk(item_begin), 0);  // the first chunk (waited in P1(0))
+    if (MODE != kModeInit && !(pa.dbg & 65)) w_fetch(item_chunk(d, item_begin), 0);  // the first chunk (waited in P1(0))
     for (int f = 0; f < nbuf - 1 && f < ntile; ++f) load_next_x(f);  // X(0 .. nbuf−2) in flight
     {
       const int xb0 = x_wait();
