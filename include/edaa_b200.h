@@ -160,6 +160,13 @@ EDAA_API int edaa_set_pixel_shard(edaa_ctx* ctx, const void* id, size_t bytes, i
 EDAA_API int edaa_shard_pixels(edaa_ctx* ctx, size_t* first, size_t* end);
 EDAA_API int edaa_set_shard_emulation(edaa_ctx* ctx, int world);
 
+/* Order of the pass kernels' (pixel slice, run chunk) work items (no reference
+ * counterpart: a scheduling knob of this implementation).  0 = auto (chunk-major
+ * when X fits in L2, else slice-major), 1 = chunk-major, 2 = slice-major.  The
+ * per-(slice, chunk) partials, and so every result, are bitwise the same for
+ * all orders; only the speed differs. */
+EDAA_API int edaa_set_pass_order(edaa_ctx* ctx, int order);
+
 /* Single-evaluation primitives on the image of the context (reference
  * solver.hpp:52-67,85-86 and ensemble.hpp:50).  Host arrays in the
  * reference layouts (b: N×p, a: p×N, e: L×p); entries follow the reference's

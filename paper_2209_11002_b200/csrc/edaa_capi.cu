@@ -84,6 +84,7 @@ struct edaa_ctx {
   ncclComm_t comm = nullptr;
   int shard_rank = 0, shard_world = 1;
   int shard_emulate = 0;  // > 1: run the slice ranges of that many ranks one after another here
+  int pass_order = 0;     // pass item order: 0 auto, 1 chunk-major, 2 slice-major (edaa_set_pass_order)
 };
 
 namespace {
@@ -332,9 +333,11 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.ncta = c->num_sms;
   d.pdl = (d.NCH * (d.sl1 - d.sl0) < c->num_sms) ? 1 : 0;
   // Chunk-major pass items when X is comfortably L2-resident (126 MB L2 on B200,
-  // shared with the slice partials); EDAA_SLICE_MAJOR=1 forces slice-major.
-  static const bool slice_major = std::getenv("EDAA_SLICE_MAJOR") != nullptr;
-  d.cmajor = (!slice_major && static_cast<size_t>(d.Lpad) * d.Npad * d.xbytes <= (size_t(96) << 20)) ? 1 : 0;
+  // shared with the slice partials), unless edaa_set_pass_order picks one.
+  if (c->pass_order == 1 || c->pass_order == 2)
+    d.cmajor = (c->pass_order == 1) ? 1 : 0;
+  else
+    d.cmajor = (static_cast<size_t>(d.Lpad) * d.Npad * d.xbytes <= (size_t(96) << 20)) ? 1 : 0;
   // X ring depth and W chunk buffers, the deepest that fits shared memory.
   static const int kRing[][2] = {{4, 2}, {3, 2}, {3, 1}, {2, 2}, {2, 1}};
   for (const auto& rw : kRing) {
@@ -1025,6 +1028,13 @@ int edaa_finish(edaa_ctx* c) {
     }
     cudaMemset(c->kprof_buf, 0, sizeof v);
   }
+  return EDAA_OK;
+}
+
+int edaa_set_pass_order(edaa_ctx* c, int order) {
+  if (!c) return EDAA_ERR_INVALID;
+  if (order < 0 || order > 2) return set_err(c, EDAA_ERR_INVALID, "pass order must be 0 (auto), 1 or 2");
+  c->pass_order = order;
   return EDAA_OK;
 }
 

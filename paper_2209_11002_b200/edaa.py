@@ -341,6 +341,11 @@ class Device:
         device (the sharded decomposition without a collective); 0 or 1 turns it off."""
         self._check(self.lib.edaa_set_shard_emulation(self.h, int(world)))
 
+    def set_pass_order(self, order: int):
+        """Pass work-item order: 0 auto, 1 chunk-major, 2 slice-major (results are
+        bitwise identical; include/edaa_b200.h)."""
+        self._check(self.lib.edaa_set_pass_order(self.h, int(order)))
+
     # -- instrumentation ---------------------------------------------------------
     def profile_enable(self, on: bool = True):
         self._check(self.lib.edaa_profile_enable(self.h, int(on)))

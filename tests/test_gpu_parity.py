@@ -377,3 +377,24 @@ def test_captured_schedule_replays_on_new_image_contents():
     r1b = edaa.run(x1, cfg)
     assert np.array_equal(r1b.objective_trace, r1.objective_trace)
     assert np.array_equal(r1b.abundances, r1.abundances)
+
+
+@pytest.mark.parametrize("runs,p", [(13, 4), (5, 12)])
+def test_pass_item_order_is_bitwise_invisible(runs, p):
+    """Chunk-major and slice-major pass schedules compute the same per-(slice, chunk)
+    partials, so traces and factors are bitwise equal (edaa_set_pass_order)."""
+    x = synth.small_scene(41, 2600, p, seed=31)
+    cfg = edaa.EnsembleConfig(runs=runs, solver=edaa.SolverConfig(endmembers=p, outer_iters=8))
+    seeds, gammas = edaa.ensemble_plan(cfg)
+    d = dev()
+    out = []
+    try:
+        for order in (1, 2):
+            d.set_pass_order(order)
+            out.append(_solve_all(d, x, p, 8, seeds, gammas))
+    finally:
+        d.set_pass_order(0)
+    (f1, t1, fit1), (f2, t2, fit2) = out
+    assert np.array_equal(t1, t2) and fit1 == fit2
+    for u, v in zip(f1, f2):
+        assert all(np.array_equal(a, b) for a, b in zip(u, v))
