@@ -98,6 +98,11 @@ EDAA_API void* edaa_stream(edaa_ctx* ctx);
  * one CTA per SM instead of two). */
 EDAA_API int edaa_set_image_host(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels);
 EDAA_API int edaa_set_image_host_f64(edaa_ctx* ctx, const double* x, size_t bands, size_t pixels);
+/* _host_checked: as _host, then HsiImage::validate (image.cpp:10-27) on the
+ * device — EDAA_ERR_INVALID with the reference's message ("image: non-finite
+ * reflectance" / "image: negative reflectance", whichever element comes first
+ * in row-major order) when the image is not finite and non-negative. */
+EDAA_API int edaa_set_image_host_checked(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels);
 EDAA_API int edaa_set_image_device(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels, size_t ld);
 
 /* Ingest on the device: HsiImage::validate + l2_normalize

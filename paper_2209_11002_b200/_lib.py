@@ -51,6 +51,7 @@ SIGNATURES = [
     ("edaa_stream", C.c_void_p, [C.c_void_p]),
     ("edaa_set_image_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t]),
     ("edaa_set_image_host_f64", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t]),
+    ("edaa_set_image_host_checked", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t]),
     ("edaa_set_image_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
                                         C.c_size_t]),
     ("edaa_ingest_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p,

@@ -181,6 +181,24 @@ __global__ void k_ingest(const double* raw, double* xn, int L, int N, int Npad, 
   if (!exact) atomicOr(inexact, 1u);
 }
 
+// HsiImage::validate (image.cpp:10-27) of an uploaded fp32 image on the device:
+// the first non-finite and the first negative element in the reference's
+// row-major L×N scan order (atomicMin of the flat index; clean images issue no
+// atomics).  Padding columns j ≥ N are skipped.
+__global__ void k_check_f32(const float* X, int L, int N, int Npad, unsigned long long* bad) {
+  const size_t total = static_cast<size_t>(L) * Npad;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / Npad), j = static_cast<int>(e - static_cast<size_t>(i) * Npad);
+    if (j >= N) continue;
+    const float v = X[e];
+    if (!isfinite(v))
+      atomicMin(bad + 0, static_cast<unsigned long long>(i) * N + j);
+    else if (v < 0.0f)
+      atomicMin(bad + 1, static_cast<unsigned long long>(i) * N + j);
+  }
+}
+
 __global__ void k_to_f32(const double* src, float* dst, size_t n) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -881,6 +899,26 @@ static int upload_host(edaa_ctx* c, const void* x, size_t bands, size_t pixels, 
 
 int edaa_set_image_host(edaa_ctx* c, const float* x, size_t bands, size_t pixels) {
   return upload_host(c, x, bands, pixels, 4);
+}
+
+int edaa_set_image_host_checked(edaa_ctx* c, const float* x, size_t bands, size_t pixels) {
+  int rc = upload_host(c, x, bands, pixels, 4);
+  if (rc) return rc;
+  cudaStream_t st = c->stream;
+  EDAA_CUDA(c, ensure(c->in_bad, 24));
+  unsigned long long* bad = P<unsigned long long>(c->in_bad);
+  EDAA_CUDA(c, cudaMemsetAsync(bad, 0xFF, 16, st));
+  const size_t total = static_cast<size_t>(c->L) * c->Npad;
+  const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, static_cast<size_t>(c->num_sms) * 8));
+  k_check_f32<<<blocks, 256, 0, st>>>(static_cast<const float*>(c->X), c->L, c->N, c->Npad, bad);
+  EDAA_CUDA(c, cudaGetLastError());
+  unsigned long long hb[2];
+  EDAA_CUDA(c, cudaMemcpyAsync(hb, bad, 16, cudaMemcpyDeviceToHost, st));
+  EDAA_CUDA(c, cudaStreamSynchronize(st));
+  if (hb[0] != ~0ull || hb[1] != ~0ull) {  // the reference throws at the first offending element
+    return set_err(c, EDAA_ERR_INVALID, hb[0] < hb[1] ? "image: non-finite reflectance" : "image: negative reflectance");
+  }
+  return EDAA_OK;
 }
 
 int edaa_set_image_host_f64(edaa_ctx* c, const double* x, size_t bands, size_t pixels) {

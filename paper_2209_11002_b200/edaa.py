@@ -152,6 +152,17 @@ def select_runs(per_run: List[RunRecord], fit_slack: float) -> SelectionReport:
     return SelectionReport(per_run, cand, best, fit_min)
 
 
+def _upload_image(dev: "Device", x) -> None:
+    """X onto the device, validated as HsiImage::validate (image.cpp:10-27) does: an
+    fp32 L×N host array is checked on the device after the upload
+    (edaa_set_image_host_checked); anything else goes through validate_image."""
+    arr = np.asarray(x)
+    if arr.ndim == 2 and arr.dtype == np.float32 and arr.shape[0] >= 1 and arr.shape[1] >= 1:
+        dev.set_image_checked(arr)
+    else:
+        dev.set_image(validate_image(arr))
+
+
 def validate_image(x) -> np.ndarray:
     """HsiImage::validate (image.cpp:10-27) on the L×N data.
 
@@ -230,6 +241,15 @@ class Device:
         return int(self.lib.edaa_stream(self.h) or 0)
 
     # -- image ------------------------------------------------------------------
+    def set_image_checked(self, x):
+        """fp32 host L×N array: upload, then HsiImage::validate on the device
+        (EdaaError with the reference's message on a non-finite or negative value)."""
+        xf = np.ascontiguousarray(x, dtype=np.float32)
+        self._x_keep = xf
+        self._check(self.lib.edaa_set_image_host_checked(self.h, xf.ctypes.data_as(C.c_void_p),
+                                                         xf.shape[0], xf.shape[1]))
+        self.L, self.N = xf.shape
+
     def set_image(self, x):
         """x: host L×N array (copied H2D) or a CUDA tensor (copied D2D)."""
         if hasattr(x, "is_cuda") and x.is_cuda:
@@ -425,9 +445,8 @@ def run(x, config: SolverConfig, observer: Optional[Callable] = None, device: in
     observer(outer, block, inner, A, B) is called after every inner step, as the
     reference's StepObserver (solver.hpp:69-77)."""
     config.validate()
-    xf = validate_image(x)
     dev = Device.get(device)
-    dev.set_image(xf)
+    _upload_image(dev, x)
     args = (config.endmembers, config.outer_iters, config.inner_iters_a, config.inner_iters_b)
     if observer is not None:
         dev.solve_observed(*args, config.seed, config.gamma, observer)
@@ -465,9 +484,8 @@ def run_ensemble(x, config: EnsembleConfig, device: int = 0):
     """Algorithm 2 (ensemble.cpp:108-167): all M runs in ONE batched device solve,
     then selection on the device.  Returns (selected RunResult, SelectionReport)."""
     config.validate()
-    xf = validate_image(x)
     dev = Device.get(device)
-    dev.set_image(xf)
+    _upload_image(dev, x)
     seeds, gammas = ensemble_plan(config)
     s = config.solver
     t0 = time.perf_counter()

@@ -398,3 +398,19 @@ def test_pass_item_order_is_bitwise_invisible(runs, p):
     assert np.array_equal(t1, t2) and fit1 == fit2
     for u, v in zip(f1, f2):
         assert all(np.array_equal(a, b) for a, b in zip(u, v))
+
+
+@pytest.mark.parametrize("first", ["negative", "non-finite"])
+def test_device_validation_reports_the_first_bad_element(first):
+    """run_ensemble on an fp32 image validates on the device (edaa_set_image_host_checked)
+    with HsiImage::validate's messages, first offending element in row-major order."""
+    x = synth.small_scene(12, 300, 3, seed=4)
+    a, b = (2, 7), (5, 3)  # a precedes b in row-major order
+    bad_a, bad_b = (-0.5, np.nan) if first == "negative" else (np.inf, -1.0)
+    x[a], x[b] = bad_a, bad_b
+    cfg = edaa.EnsembleConfig(runs=2, solver=edaa.SolverConfig(endmembers=3, outer_iters=2))
+    with pytest.raises(edaa.EdaaError, match="image: %s reflectance" % first):
+        edaa.run_ensemble(x, cfg)
+    with pytest.raises(edaa.EdaaError, match="image: %s reflectance" % first):
+        edaa.validate_image(x)  # the host restatement agrees
+    edaa.run_ensemble(synth.small_scene(12, 300, 3, seed=4), cfg)  # a clean image still solves
