@@ -488,32 +488,60 @@ template <class XT>
 __global__ void __launch_bounds__(256) k_strict_e(const XT* X, const double* Bv, double* E, Dims d) {
   // One output per thread (8 band rows × 32 columns per CTA): the pixel-ascending
   // chain is inherently sequential, so throughput comes from running many chains
-  // (L·M·p of them) on every SM at once.
-  __shared__ double xs[8][64];
-  __shared__ double bs[32][65];
+  // (L·M·p of them) on every SM at once.  The next 128-pixel chunk of X and B̂ is
+  // loaded into registers while the current one is consumed from shared memory,
+  // so the chains run at the dependent-DADD rate instead of waiting on L2 per chunk.
+  constexpr int kJ = 128;
+  constexpr int kXE = 8 * kJ / 256, kBE = 32 * kJ / 256;  // elements per thread per chunk
+  __shared__ double xs[8][kJ];
+  __shared__ double bs[32][kJ + 1];
   const int lane = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const int l0 = blockIdx.x * 8, c0 = blockIdx.y * 32;
   const int ncol = d.M * d.p;
-  double s = 0.0;
-  for (int j0 = 0; j0 < d.N; j0 += 64) {
-    for (int e = threadIdx.x; e < 8 * 64; e += 256) {
-      const int rr = e / 64, jj = e % 64;
+  double rx[kXE], rb[kBE];
+  auto fetch = [&](int j0) {
+#pragma unroll
+    for (int k = 0; k < kXE; ++k) {
+      const int e = threadIdx.x + 256 * k, rr = e / kJ, jj = e % kJ;
       const int l = l0 + rr, j = j0 + jj;
-      xs[rr][jj] = (l < d.L && j < d.N) ? static_cast<double>(X[static_cast<size_t>(l) * d.Npad + j]) : 0.0;
+      rx[k] = (l < d.L && j < d.N) ? static_cast<double>(X[static_cast<size_t>(l) * d.Npad + j]) : 0.0;
     }
-    for (int e = threadIdx.x; e < 32 * 64; e += 256) {
-      const int rr = e / 64, jj = e % 64;
+#pragma unroll
+    for (int k = 0; k < kBE; ++k) {
+      const int e = threadIdx.x + 256 * k, rr = e / kJ, jj = e % kJ;
       const int c = c0 + rr, j = j0 + jj;
-      bs[rr][jj] = (c < ncol && j < d.N) ? Bv[static_cast<size_t>(c) * d.Npad + j] : 0.0;
+      rb[k] = (c < ncol && j < d.N) ? Bv[static_cast<size_t>(c) * d.Npad + j] : 0.0;
     }
-    __syncthreads();
-    if (d.N - j0 >= 64) {
+  };
+  auto stage = [&]() {
+#pragma unroll
+    for (int k = 0; k < kXE; ++k) {
+      const int e = threadIdx.x + 256 * k;
+      xs[e / kJ][e % kJ] = rx[k];
+    }
+#pragma unroll
+    for (int k = 0; k < kBE; ++k) {
+      const int e = threadIdx.x + 256 * k;
+      bs[e / kJ][e % kJ] = rb[k];
+    }
+  };
+  double s = 0.0;
+  fetch(0);
+  stage();
+  __syncthreads();
+  for (int j0 = 0; j0 < d.N; j0 += kJ) {
+    if (j0 + kJ < d.N) fetch(j0 + kJ);  // in flight during the chain below
+    if (d.N - j0 >= kJ) {
 #pragma unroll 16
-      for (int jj = 0; jj < 64; ++jj) s = __dadd_rn(s, __dmul_rn(xs[ry][jj], bs[lane][jj]));
+      for (int jj = 0; jj < kJ; ++jj) s = __dadd_rn(s, __dmul_rn(xs[ry][jj], bs[lane][jj]));
     } else {
       for (int jj = 0; jj < d.N - j0; ++jj) s = __dadd_rn(s, __dmul_rn(xs[ry][jj], bs[lane][jj]));
     }
     __syncthreads();
+    if (j0 + kJ < d.N) {
+      stage();
+      __syncthreads();
+    }
   }
   const int c = c0 + lane;
   const int l = l0 + ry;
