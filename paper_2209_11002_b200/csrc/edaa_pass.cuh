@@ -71,7 +71,8 @@ struct LanesPerPixel {
 template <int PT, int TPP, bool UPDATE, bool EXACT>
 __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int rl, int j, int pix,
                                                  bool valid, int sub, double* ss, const double* sh,
-                                                 const double* st, const double* gs, const double* T) {
+                                                 const double* st, const double* gs, const double* T,
+                                                 const double* ceta) {
   // EXACT: p == PT, so every index below is compile-time except the lane's `sub`.
   constexpr int EPT = (PT + TPP - 1) / TPP;
   constexpr bool kAllValid = EXACT && (PT % TPP == 0);
@@ -80,7 +81,7 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
   const int p = EXACT ? PT : d.p;
   const int gbase = (threadIdx.x & 31) - sub;
   const double xn = valid ? pa.xnorm[pix] : 0.0;
-  const double eta = pa.eta_a[r];
+  const double eta = ceta[rl];  // η_a of the run, staged in shared memory at the chunk change
   double a[EPT], P[EPT];
   bool own[EPT];
 #pragma unroll
@@ -702,7 +703,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           const bool real = c < ci.ncol;
           // log b_old = ℓ − (m + log S): one subtraction per element
           c_m[c] = (MODE == kModeB && real) ? pa.colm[ci.col0 + c] + pa.collogS[ci.col0 + c] : 0.0;
-          c_eta[c] = (MODE == kModeB && real) ? pa.eta_b[ci.run0 + c / p] : 0.0;
+          c_eta[c] = (MODE == kModeB && real) ? pa.eta_b[ci.run0 + c / p]
+                     : ((MODE == kModeA && c < ci.RCe) ? pa.eta_a[ci.run0 + c] : 0.0);  // B: per column, A: per run
         }
         if (MODE == kModeA || MODE == kModeObj) {
           for (int e = gtid; e < ci.RCe * p * p; e += kGroup) {
@@ -742,9 +744,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           const int pix = j0 + j;
           double o = (p == PT)
               ? pixel_a_update<PT, TPP, MODE == kModeA, true>(pa, ci.run0 + rl, rl, j, pix, pix < d.N, sub,
-                                                              ss, sh, st, gs, etab)
+                                                              ss, sh, st, gs, etab, c_eta)
               : pixel_a_update<PT, TPP, MODE == kModeA, false>(pa, ci.run0 + rl, rl, j, pix, pix < d.N, sub,
-                                                               ss, sh, st, gs, etab);
+                                                               ss, sh, st, gs, etab, c_eta);
           o = warp_sum(o);
           if (lane == 0) hobj[q2 >> 5] = o;  // warp-task q2/32 belongs to run (q2/32)/TPP
         }
