@@ -223,7 +223,7 @@ constexpr int kXRow = 128 / sizeof(XT);
 // tiles and k-steps are compile-time, so the DMMAs are unpredicated and the
 // swizzled X addresses reduce to a per-k-step table (row & 7 == g for every
 // fragment row).
-template <int R, bool PSEUDO, int RTW, class XT>
+template <int R, bool PSEUDO, int CT, int RTW, class XT>
 __device__ __forceinline__ void accumulate_tiles(double (&ac)[RTW][kMaxCT][2], const XT* xs,
                                                  const double* w, int gwarp, int nRTx, int g, int t4,
                                                  const int (&xo)[kNP / 4]) {
@@ -231,19 +231,19 @@ __device__ __forceinline__ void accumulate_tiles(double (&ac)[RTW][kMaxCT][2], c
   const double* prow = w + ((gwarp + 8 * R - nRTx) * 8 + g) * kSST + t4;  // the pseudo tile's rows
 #pragma unroll
   for (int kk = 0; kk < kNP / 4; ++kk) {
-    double bw[kMaxCT];
+    double bw[CT];
 #pragma unroll
-    for (int ct = 0; ct < kMaxCT; ++ct) bw[ct] = wrow[ct * 8 * kSST + kk * 4];
+    for (int ct = 0; ct < CT; ++ct) bw[ct] = wrow[ct * 8 * kSST + kk * 4];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const double ax = static_cast<double>(xs[(gwarp + 8 * i) * 8 * kXRow<XT> + xo[kk]]);
 #pragma unroll
-      for (int ct = 0; ct < kMaxCT; ++ct) dmma(ac[i][ct], ax, bw[ct]);
+      for (int ct = 0; ct < CT; ++ct) dmma(ac[i][ct], ax, bw[ct]);
     }
     if constexpr (PSEUDO) {
       const double ax = prow[kk * 4];
 #pragma unroll
-      for (int ct = 0; ct < kMaxCT; ++ct) dmma(ac[R][ct], ax, bw[ct]);
+      for (int ct = 0; ct < CT; ++ct) dmma(ac[R][ct], ax, bw[ct]);
     }
   }
 }
@@ -337,7 +337,10 @@ __device__ __forceinline__ ChunkInfo chunk_info(const Dims& d, int chunk) {
   return ci;
 }
 
-template <int MODE, int PT, int RTW, class XT>
+// CTF: DMMA column tiles computed per chunk — kMaxCT, or 1 when the whole batch
+// fits one 8-column tile (a single run with p ≤ 8: cfg0, the pixel-sharded run),
+// which skips the DMMAs of the empty tiles (their w is 0, their partials stay 0).
+template <int MODE, int PT, int RTW, class XT, int CTF>
 __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(16) unsigned char smem[];
   const long long t_kernel0 = pa.kprof ? clock64() : 0;
@@ -519,9 +522,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       const double* ws = ws_buf(wcur);
       const XT* xs = xslot(xb);
       const int pt = p1_pt, half = p1_half;
-      double c1[kMaxCT][2];
+      double c1[CTF][2];
 #pragma unroll
-      for (int c = 0; c < kMaxCT; ++c) c1[c][0] = c1[c][1] = 0.0;
+      for (int c = 0; c < CTF; ++c) c1[c][0] = c1[c][1] = 0.0;
       // Bands are taken in pairs of k-steps covering 8 bands: within pair m, lane
       // (g, t4) feeds band 8m + 2·t4 + par (par = 0, 1).  This band order makes
       // both the X B-fragment (rows 2·t4+par hit distinct 128-byte swizzle chunks)
@@ -539,13 +542,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         const double* w0 = wcol + m * 8 * WST;
         const double* w1 = w0 + WST;
 #pragma unroll
-        for (int ct = 0; ct < kMaxCT; ++ct) dmma(c1[ct], w0[ct * 8], bx0);
+        for (int ct = 0; ct < CTF; ++ct) dmma(c1[ct], w0[ct * 8], bx0);
 #pragma unroll
-        for (int ct = 0; ct < kMaxCT; ++ct) dmma(c1[ct], w1[ct * 8], bx1);
+        for (int ct = 0; ct < CTF; ++ct) dmma(c1[ct], w1[ct * 8], bx1);
       }
       double* dst = half ? hbuf(i) : sbuf(i);
 #pragma unroll
-      for (int ct = 0; ct < kMaxCT; ++ct)
+      for (int ct = 0; ct < CTF; ++ct)
         *reinterpret_cast<double2*>(dst + (ct * 8 + g) * kSST + pt * 8 + 2 * t4) =
             make_double2(c1[ct][0], c1[ct][1]);
     };
@@ -616,18 +619,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         EDAA_TSTART();
         if (!(pa.dbg & 129)) {
           switch (my_x + (my_pseudo ? 8 : 0)) {  // warp-uniform: the DMMAs below are unpredicated
-            case 1: accumulate_tiles<1, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 2: accumulate_tiles<2, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 3: accumulate_tiles<3, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 4: if constexpr (RTW >= 4) accumulate_tiles<4, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 5: if constexpr (RTW >= 5) accumulate_tiles<5, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 6: if constexpr (RTW >= 6) accumulate_tiles<6, false>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 8: if constexpr (MODE == kModeA) accumulate_tiles<0, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 9: if constexpr (MODE == kModeA) accumulate_tiles<1, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 10: if constexpr (MODE == kModeA) accumulate_tiles<2, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 11: if constexpr (MODE == kModeA) accumulate_tiles<3, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 12: if constexpr (MODE == kModeA && RTW >= 5) accumulate_tiles<4, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
-            case 13: if constexpr (MODE == kModeA && RTW >= 6) accumulate_tiles<5, true>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 1: accumulate_tiles<1, false, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 2: accumulate_tiles<2, false, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 3: accumulate_tiles<3, false, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 4: if constexpr (RTW >= 4) accumulate_tiles<4, false, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 5: if constexpr (RTW >= 5) accumulate_tiles<5, false, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 6: if constexpr (RTW >= 6) accumulate_tiles<6, false, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 8: if constexpr (MODE == kModeA) accumulate_tiles<0, true, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 9: if constexpr (MODE == kModeA) accumulate_tiles<1, true, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 10: if constexpr (MODE == kModeA) accumulate_tiles<2, true, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 11: if constexpr (MODE == kModeA) accumulate_tiles<3, true, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 12: if constexpr (MODE == kModeA && RTW >= 5) accumulate_tiles<4, true, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
+            case 13: if constexpr (MODE == kModeA && RTW >= 6) accumulate_tiles<5, true, CTF>(acc, xs, w, gwarp, nRTx, g, t4, xo3); break;
             default: break;
           }
         }
@@ -835,18 +838,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
 // carry different bucket sets never define the same function differently.
 enum PtSet : int { kPtAll = 0, kPtLo = 1, kPtHi = 2 };
 
-template <int MODE, int RTW, class XT, int PTS>
-cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
+template <int MODE, int RTW, class XT, int PTS, int CTF>
+cudaError_t launch_pass_ctf(const PassArgs& a, cudaStream_t st, int pt) {
   const dim3 grid(std::min(a.d.NCH * (a.d.sl1 - a.d.sl0), a.d.ncta));
   const size_t smem = dev::smem_layout(a.d, a.d.nbuf).total;
   void (*kern)(PassArgs, CUtensorMap) = nullptr;
   if constexpr (MODE == kModeInit || MODE == kModeB) {
-    kern = k_pass<MODE, 1, RTW, XT>;
+    kern = k_pass<MODE, 1, RTW, XT, CTF>;
   } else {
     switch (pt) {
-#define EDAA_PT_CASE(P)                                                                     \
-  case P:                                                                                   \
-    if constexpr (PTS == kPtAll || (PTS == kPtLo) == (P <= 5)) kern = k_pass<MODE, P, RTW, XT>; \
+#define EDAA_PT_CASE(P)                                                                         \
+  case P:                                                                                       \
+    if constexpr ((PTS == kPtAll || (PTS == kPtLo) == (P <= 5)) && (CTF == kMaxCT || P <= 8)) \
+      kern = k_pass<MODE, P, RTW, XT, CTF>;                                                    \
     break;
       EDAA_PT_CASE(2) EDAA_PT_CASE(3) EDAA_PT_CASE(4) EDAA_PT_CASE(5)
       EDAA_PT_CASE(6) EDAA_PT_CASE(7) EDAA_PT_CASE(8) EDAA_PT_CASE(10) EDAA_PT_CASE(12) EDAA_PT_CASE(16)
@@ -864,6 +868,13 @@ cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
   return cudaGetLastError();
 }
 
+// A batch that fits one 8-column DMMA tile (a single run with p ≤ 8) runs the
+// CTF = 1 kernels; every other batch the full-chunk ones.
+template <int MODE, int RTW, class XT, int PTS>
+cudaError_t launch_pass_rtw(const PassArgs& a, cudaStream_t st, int pt) {
+  return (a.d.NCH == 1 && a.d.M * a.d.p <= 8) ? launch_pass_ctf<MODE, RTW, XT, PTS, 1>(a, st, pt)
+                                              : launch_pass_ctf<MODE, RTW, XT, PTS, kMaxCT>(a, st, pt);
+}
 
 // Per-mode entry points: each translation unit edaa_pass_<x>_<part>.cu instantiates
 // one (image type, mode, p-bucket range) so the kernels compile in parallel.
