@@ -76,7 +76,7 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
   // EXACT: p == PT, so every index below is compile-time except the lane's `sub`.
   constexpr int EPT = (PT + TPP - 1) / TPP;
   constexpr bool kAllValid = EXACT && (PT % TPP == 0);
-  constexpr bool kGinRegs = EXACT && EPT * PT <= 48;  // the lane's rows of G stay in registers
+  constexpr bool kGinRegs = EXACT && EPT * PT <= 24;  // the lane's rows of G stay in registers (larger: smem; p = 7, 8 spilled)
   const Dims& d = pa.d;
   const int p = EXACT ? PT : d.p;
   const int gbase = (threadIdx.x & 31) - sub;
