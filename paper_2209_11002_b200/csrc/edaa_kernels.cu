@@ -593,18 +593,29 @@ __global__ void k_fit_final(const double* part, double* fit, int nblk, int M) {
 
 // coherence (ensemble.cpp:41-60): raw max_{i<j} ⟨e_i, e_j⟩, reference order.
 __global__ void k_coherence(const double* E, double* mu, Dims d) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  // One warp per run, one lane per endmember pair (i < j): each dot product keeps
+  // the reference's band-ascending multiply-then-add chain (ensemble.cpp:41-60), and
+  // the max over pairs is order-free (std::max semantics: NaN dots never win).
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (r >= d.M) return;
-  const int p = d.p;
+  const int p = d.p, npair = p * (p - 1) / 2;
   const double* e = E + static_cast<size_t>(r) * d.Lpad * p;
   double best = -INFINITY;
-  for (int i = 0; i < p; ++i)
-    for (int j = i + 1; j < p; ++j) {
-      double dot = 0.0;
-      for (int l = 0; l < d.L; ++l) dot = __dadd_rn(dot, __dmul_rn(e[l * p + i], e[l * p + j]));
-      best = max_like_std(best, dot);
+  for (int q = lane; q < npair; q += 32) {
+    int i = 0, rem = q;
+    while (rem >= p - 1 - i) {
+      rem -= p - 1 - i;
+      ++i;
     }
-  mu[r] = (best == -INFINITY) ? 0.0 : best;
+    const int j = i + 1 + rem;
+    double dot = 0.0;
+    for (int l = 0; l < d.L; ++l) dot = __dadd_rn(dot, __dmul_rn(e[l * p + i], e[l * p + j]));
+    best = max_like_std(best, dot);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = max_like_std(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (lane == 0) mu[r] = (best == -INFINITY) ? 0.0 : best;
 }
 
 // select_runs (ensemble.cpp:71-94) on device: fit_min over ok runs, cutoff
@@ -735,7 +746,7 @@ cudaError_t launch_fit(const void* X, const double* E, const double* A, double* 
 }
 
 cudaError_t launch_coherence(const double* E, double* mu, const Dims& d, cudaStream_t st) {
-  k_coherence<<<(d.M + 63) / 64, 64, 0, st>>>(E, mu, d);
+  k_coherence<<<(d.M + 3) / 4, 128, 0, st>>>(E, mu, d);
   return cudaGetLastError();
 }
 
