@@ -26,10 +26,17 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisib
                   "-I" + os.path.join(ROOT, "include")]
 CUDA_SRCS = (["edaa_pass_%s_%s.cu" % (x, m) for x in ("f32", "f64") for m in ("alo", "ahi", "b", "init", "obj")]
              + ["edaa_kernels.cu", "edaa_prims.cu", "edaa_capi.cu"])
-HOST_SRCS = ["matrix.cpp", "image.cpp", "types.cpp", "solver.cpp", "ensemble.cpp", "device.cpp"]
+HOST_SRCS = ["matrix.cpp", "image.cpp", "types.cpp", "solver.cpp", "ensemble.cpp", "device.cpp",
+             # the formats and the front end either side of the path
+             "npy.cpp", "envi.cpp", "metrics.cpp", "outputs.cpp", "synth.cpp", "cli.cpp"]
+# nlohmann/json (the reference's JSON dependency, vendor/json.hpp there) from the
+# image's third-party copy; report.json byte-compatibility depends on it.
+JSON_INC = os.path.join(__import__("sysconfig").get_paths()["purelib"],
+                        "include", "cudnn_frontend", "thirdparty", "nlohmann")
 
 CUDA_LIB = os.path.join(PKG, "libedaa_cuda.so")
 HOST_LIB = os.path.join(PKG, "libarchetype_b200.so")
+CLI_BIN = os.path.join(PKG, "archetype")  # the reference's tools/main.cpp equivalent
 
 
 def _run(cmd):
@@ -74,9 +81,25 @@ def build_host(force=False):
     hdr_dir = os.path.join(ROOT, "include", "archetype")
     deps = hsrc + [os.path.join(hdr_dir, h) for h in os.listdir(hdr_dir)] + [CUDA_LIB]
     if force or _stale(HOST_LIB, deps):
-        _run(["g++", "-std=c++20", "-O3", "-DNDEBUG", "-fPIC", "-shared",
-              "-I" + os.path.join(ROOT, "include"), "-o", HOST_LIB] + hsrc +
+        objs = []
+        jobs = []
+        os.makedirs(BUILD, exist_ok=True)
+        for src in hsrc:
+            obj = os.path.join(BUILD, "host_" + os.path.basename(src) + ".o")
+            objs.append(obj)
+            jobs.append(["g++", "-std=c++20", "-O3", "-DNDEBUG", "-fPIC", "-Wall",
+                         "-I" + os.path.join(ROOT, "include"), "-I" + JSON_INC, "-c", src, "-o", obj])
+        with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+            list(ex.map(_run, jobs))
+        _run(["g++", "-shared", "-o", HOST_LIB] + objs +
              ["-L" + PKG, "-ledaa_cuda", "-Wl,-rpath,$ORIGIN", "-lpthread"])
+    if force or _stale(CLI_BIN, [HOST_LIB]):
+        main = os.path.join(BUILD, "archetype_main.cpp")
+        with open(main, "w") as f:
+            f.write('#include "archetype/cli.hpp"\n'
+                    'int main(int argc, char** argv) { return archetype::cli_main(argc, argv); }\n')
+        _run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), "-o", CLI_BIN, main,
+              "-L" + PKG, "-larchetype_b200", "-ledaa_cuda", "-Wl,-rpath,$ORIGIN", "-lpthread"])
     return HOST_LIB
 
 

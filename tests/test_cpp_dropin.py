@@ -23,11 +23,21 @@ API = ["archetype::run(", "archetype::run_ensemble(", "archetype::select_runs(",
        "archetype::matmul(", "archetype::matmul_tn(", "archetype::matmul_nt(",
        "archetype::spectral_norm(", "archetype::l2_normalize(",
        "archetype::SolverConfig::validate()", "archetype::EnsembleConfig::validate()",
-       "archetype::HsiImage::validate()", "archetype::validate_simplex_columns("]
+       "archetype::HsiImage::validate()", "archetype::validate_simplex_columns(",
+       # formats, output bundle, scoring, generator, front end
+       "archetype::read_npy(", "archetype::write_npy(", "archetype::npy_to_matrix(",
+       "archetype::npy_to_image(", "archetype::read_envi(", "archetype::envi_data_path(",
+       "archetype::report_to_json(", "archetype::report_from_json(", "archetype::evaluation_to_json(",
+       "archetype::write_csv_endmembers(", "archetype::read_csv_endmembers(", "archetype::write_pgm(",
+       "archetype::write_outputs(", "archetype::evaluate_unmixing(", "archetype::match_endmembers(",
+       "archetype::min_cost_assignment(", "archetype::spectral_angle_deg(", "archetype::rmse_percent(",
+       "archetype::sad_degrees(", "archetype::format_evaluation(", "archetype::generate(",
+       "archetype::cli_main("]
 
 
 def test_library_exports_reference_api():
     out = subprocess.run(["nm", "-DC", "--defined-only", LIB], capture_output=True, text=True).stdout
+    out = out.replace("[abi:cxx11]", "")  # functions returning std::string carry the ABI tag
     for sym in API:
         assert sym in out, sym
 
@@ -45,6 +55,41 @@ def test_restated_reference_unit_tests_pass_on_gpu():
     print(r.stderr)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "A/B" in r.stdout
+
+
+CLI_TEST = os.path.join(ROOT, "tests", "cpp", "build", "test_cli")
+CLI_BIN = os.path.join(ROOT, "paper_2209_11002_b200", "archetype")
+
+
+@pytest.mark.gpu
+def test_cli_unmix_pipeline_on_gpu():
+    """tests/cpp/test_cli.cpp [gpu] cases (the reference's test_cli.cpp:167-250):
+    synth → unmix (one batched GPU solve of 50 runs) → evaluate recovers the
+    planted endmembers; report.json replays the selected run bitwise through
+    archetype::run; spatial cubes get PGM maps."""
+    r = subprocess.run([CLI_TEST, "gpu:"], capture_output=True, text=True, cwd=ROOT, timeout=600)
+    print(r.stdout)
+    print(r.stderr)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "0 failures" in r.stdout and "[ ok ] gpu: report fields replay" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cli_binary_runs_unmix_end_to_end(tmp_path):
+    """The shipped `archetype` executable (the reference's tools/main.cpp)."""
+    run = lambda *a: subprocess.run([CLI_BIN, *map(str, a)], capture_output=True, text=True, timeout=300)
+    s = run("synth", "--bands", 16, "--pixels", 300, "--endmembers", 3, "--snr", 40, "--seed", 4,
+            "--output", tmp_path / "fx")
+    assert s.returncode == 0, s.stderr
+    u = run("unmix", "--input", tmp_path / "fx" / "cube.npy", "--endmembers", 3, "--runs", 8,
+            "--outer", 30, "--output", tmp_path / "est")
+    assert u.returncode == 0, u.stderr
+    assert "selected: run" in u.stdout
+    for f in ("endmembers.csv", "abundances.npy", "report.json"):
+        assert (tmp_path / "est" / f).exists()
+    e = run("evaluate", "--est", tmp_path / "est", "--gt-endmembers", tmp_path / "fx" / "endmembers.csv",
+            "--gt-abundances", tmp_path / "fx" / "abundances.npy")
+    assert e.returncode == 0 and "overall" in e.stdout, e.stderr
 
 
 ACC = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
