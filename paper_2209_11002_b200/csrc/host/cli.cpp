@@ -31,6 +31,7 @@
 #include "archetype/solver.hpp"
 #include "archetype/synth.hpp"
 #include "archetype/version.hpp"
+#include "device.hpp"
 
 namespace archetype {
 
@@ -180,8 +181,6 @@ struct UnmixArgs {
 
 int unmix(const UnmixArgs& args, std::ostream& out) {
   const HsiImage cube = load_cube(args.input);
-  cube.validate();
-  const NormalizeResult norm = l2_normalize(cube);
 
   RunReport report;
   report.version = kVersion;
@@ -189,7 +188,6 @@ int unmix(const UnmixArgs& args, std::ostream& out) {
   report.bands = cube.bands();
   report.pixels = cube.pixels();
   report.spatial = cube.spatial;
-  report.zero_pixels = norm.zero_pixels.size();
   EnsembleConfig& cfg = report.config;
   cfg.runs = args.runs;
   cfg.base_seed = args.seed;
@@ -200,7 +198,19 @@ int unmix(const UnmixArgs& args, std::ostream& out) {
   cfg.solver.inner_iters_a = args.inner;
   cfg.solver.inner_iters_b = args.inner;
 
-  auto solved = run_ensemble(norm.image, cfg);  // all runs: one batched GPU solve
+  // validate → ℓ2-normalise → all M runs as one batched GPU solve. The
+  // normalisation runs in the device ingest (the reference's bits and
+  // messages); ARCHETYPE_HOST_NORMALIZE=1 takes the host fp64 route instead.
+  std::pair<RunResult, SelectionReport> solved;
+  const char* host_norm = std::getenv("ARCHETYPE_HOST_NORMALIZE");
+  if (host_norm && *host_norm && std::string(host_norm) != "0") {
+    cube.validate();
+    const NormalizeResult norm = l2_normalize(cube);
+    report.zero_pixels = norm.zero_pixels.size();
+    solved = run_ensemble(norm.image, cfg);
+  } else {
+    solved = detail::run_ensemble_raw(cube, cfg, report.zero_pixels);
+  }
   report.selection = std::move(solved.second);
   write_outputs(args.output, solved.first, report);
 

@@ -4,8 +4,13 @@
 #include <mutex>
 #include <string>
 
+#include <utility>
+
+#include "archetype/ensemble.hpp"
 #include "archetype/error.hpp"
+#include "archetype/image.hpp"
 #include "archetype/matrix.hpp"
+#include "archetype/solver.hpp"
 #include "edaa_b200.h"
 
 namespace archetype::detail {
@@ -25,5 +30,12 @@ Device& device(int i);
 /// Copies X to the device: fp32 when every entry is exactly an fp32 (fast
 /// path), fp64 otherwise.
 void upload_image(Device& d, const Matrix& x);
+
+/// run_ensemble(l2_normalize(raw).image, config) with the validate + ℓ2
+/// normalisation done by the device ingest (edaa_ingest_host: same bits, same
+/// messages in the same order) instead of host fp64 passes; `zero_pixels`
+/// receives NormalizeResult::zero_pixels.size(). The CLI's `unmix` path.
+std::pair<RunResult, SelectionReport> run_ensemble_raw(const HsiImage& raw, const EnsembleConfig& config,
+                                                       std::size_t& zero_pixels);
 
 }  // namespace archetype::detail

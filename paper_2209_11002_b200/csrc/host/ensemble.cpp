@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <exception>
+#include <functional>
 #include <limits>
 #include <thread>
 
@@ -104,12 +105,14 @@ struct Shard {
   std::exception_ptr error;
 };
 
-void solve_shard(Shard& sh, const HsiImage& x, const EnsembleConfig& cfg,
+using Uploader = std::function<void(detail::Device&)>;
+
+void solve_shard(Shard& sh, const Uploader& upload, const EnsembleConfig& cfg,
                  const std::vector<std::uint64_t>& seeds, const std::vector<double>& gammas) {
   try {
     detail::Device& d = *sh.dev;
     std::lock_guard<std::mutex> lock(d.mu);
-    detail::upload_image(d, x.data);
+    upload(d);
     const edaa_solve_params prm{cfg.solver.endmembers, cfg.solver.outer_iters,
                                 cfg.solver.inner_iters_a, cfg.solver.inner_iters_b, sh.count,
                                 seeds.data() + sh.first, gammas.data() + sh.first};
@@ -126,10 +129,12 @@ void solve_shard(Shard& sh, const HsiImage& x, const EnsembleConfig& cfg,
 
 }  // namespace
 
-std::pair<RunResult, SelectionReport> run_ensemble(const HsiImage& x,
-                                                   const EnsembleConfig& config) {
-  config.validate();
-  x.validate();
+namespace {
+
+// The batched solve behind run_ensemble, for an image the uploader puts on
+// every device (host-normalised X, or the raw cube through the device ingest).
+std::pair<RunResult, SelectionReport> ensemble_on_devices(const Uploader& upload, std::size_t l,
+                                                          std::size_t n, const EnsembleConfig& config) {
   const std::size_t M = config.runs;
   std::vector<std::uint64_t> seeds(M);
   std::vector<double> gammas(M);
@@ -146,10 +151,10 @@ std::pair<RunResult, SelectionReport> run_ensemble(const HsiImage& x,
     shards[g].dev = &detail::device(static_cast<int>(g));
   }
   if (ndev == 1) {
-    solve_shard(shards[0], x, config, seeds, gammas);
+    solve_shard(shards[0], upload, config, seeds, gammas);
   } else {
     std::vector<std::thread> pool;
-    for (auto& sh : shards) pool.emplace_back([&, ptr = &sh] { solve_shard(*ptr, x, config, seeds, gammas); });
+    for (auto& sh : shards) pool.emplace_back([&, ptr = &sh] { solve_shard(*ptr, upload, config, seeds, gammas); });
     for (auto& t : pool) t.join();
   }
   for (auto& sh : shards)
@@ -194,7 +199,7 @@ std::pair<RunResult, SelectionReport> run_ensemble(const HsiImage& x,
   Shard* owner = nullptr;
   for (auto& sh : shards)
     if (s >= sh.first && s < sh.first + sh.count) owner = &sh;
-  const std::size_t p = config.solver.endmembers, n = x.pixels(), l = x.bands();
+  const std::size_t p = config.solver.endmembers;
   RunResult res;
   res.seed = seeds[s];
   res.gamma = gammas[s];
@@ -217,5 +222,60 @@ std::pair<RunResult, SelectionReport> run_ensemble(const HsiImage& x,
   }
   return {std::move(res), std::move(report)};
 }
+
+}  // namespace
+
+std::pair<RunResult, SelectionReport> run_ensemble(const HsiImage& x,
+                                                   const EnsembleConfig& config) {
+  config.validate();
+  x.validate();
+  return ensemble_on_devices([&x](detail::Device& d) { detail::upload_image(d, x.data); }, x.bands(),
+                             x.pixels(), config);
+}
+
+namespace detail {
+
+// HsiImage::validate's non-value checks (image.cpp:15-26), in its order.
+static void check_shape(const HsiImage& raw) {
+  if (raw.spatial && raw.spatial->height * raw.spatial->width != raw.pixels()) {
+    HsiImage probe;  // the reference's message, built by the host validate
+    probe.data = Matrix(1, raw.pixels());
+    probe.spatial = raw.spatial;
+    probe.validate();
+  }
+  if (!raw.wavelengths.empty() && raw.wavelengths.size() != raw.bands())
+    throw Error("image: wavelength list length differs from band count");
+}
+
+std::pair<RunResult, SelectionReport> run_ensemble_raw(const HsiImage& raw, const EnsembleConfig& config,
+                                                       std::size_t& zero_pixels) {
+  if (raw.bands() < 1 || raw.pixels() < 1) raw.validate();  // the reference's size message
+  // Value checks + ℓ2 normalisation on the device (edaa_ingest_host) in the
+  // reference's order of messages: a bad value, then the shape checks, then
+  // "degenerate input" — all before the config is looked at, as `unmix`
+  // validates and normalises the image before run_ensemble (cli.cpp:75-78).
+  const auto ingest = [&raw](Device& d) {
+    std::size_t nz = 0;
+    if (edaa_ingest_host(d.ctx, raw.data.values().data(), raw.bands(), raw.pixels(), nullptr, 0, &nz) !=
+        EDAA_OK) {
+      const std::string what = edaa_last_error(d.ctx);
+      if (what.rfind("degenerate", 0) == 0) check_shape(raw);
+      throw Error(what);
+    }
+    return nz;
+  };
+  Device& first = device(0);
+  {
+    std::lock_guard<std::mutex> lock(first.mu);
+    zero_pixels = ingest(first);
+  }
+  check_shape(raw);
+  config.validate();
+  // Device 0 already holds the normalised image; further devices ingest their own copy.
+  return ensemble_on_devices([&](Device& d) { if (&d != &first) ingest(d); }, raw.bands(), raw.pixels(),
+                             config);
+}
+
+}  // namespace detail
 
 }  // namespace archetype

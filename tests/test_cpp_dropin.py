@@ -114,3 +114,54 @@ def test_reference_acceptance_gate_passes_on_gpu():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "all checks passed" in r.stdout
     assert r.stdout.count("PASS") >= 8
+
+
+@pytest.mark.gpu
+def test_cli_device_ingest_equals_host_normalisation(tmp_path):
+    """`unmix` normalises through the device ingest; ARCHETYPE_HOST_NORMALIZE=1
+    takes the reference's host fp64 route. The bundles are identical (but for
+    the measured wall_ms), and the error messages come in the reference's
+    order: a bad value before a bad config, a wavelength mismatch before
+    "degenerate input"."""
+    import json
+    import numpy as np
+
+    def unmix(cube, out, *extra, host=False):
+        env = dict(os.environ, ARCHETYPE_HOST_NORMALIZE="1" if host else "0")
+        return subprocess.run([CLI_BIN, "unmix", "--input", cube, "--endmembers", "3", "--runs", "6",
+                               "--outer", "15", "--output", out, *extra], capture_output=True, text=True,
+                              env=env, timeout=300)
+
+    rng = np.random.default_rng(11)
+    x = rng.random((5, 7, 19)) ** 2 + 0.01   # (H, W, L): not fp32-exact after normalising
+    x[2, 3, :] = 0.0                          # one zero pixel, left unnormalised
+    np.save(tmp_path / "cube.npy", x)
+    a = unmix(str(tmp_path / "cube.npy"), str(tmp_path / "dev"))
+    b = unmix(str(tmp_path / "cube.npy"), str(tmp_path / "host"), host=True)
+    assert a.returncode == 0 and b.returncode == 0, a.stderr + b.stderr
+    for f in ("abundances.npy", "endmembers.csv", "maps/endmember_1.pgm", "maps/endmember_3.pgm"):
+        assert (tmp_path / "dev" / f).read_bytes() == (tmp_path / "host" / f).read_bytes(), f
+    ra, rb = (json.loads((tmp_path / d / "report.json").read_text()) for d in ("dev", "host"))
+    assert ra["zero_pixels"] == rb["zero_pixels"] == 1
+    for r in ra["runs"] + rb["runs"]:
+        r.pop("wall_ms")
+    assert ra == rb
+
+    bad = x.copy()
+    bad[1, 1, 4] = -0.5
+    np.save(tmp_path / "bad.npy", bad)
+    for host in (False, True):
+        r = unmix(str(tmp_path / "bad.npy"), str(tmp_path / "o"), "--gamma-set", "0", host=host)
+        assert r.returncode == 2 and "image: negative reflectance" in r.stderr, r.stderr
+        r = unmix(str(tmp_path / "cube.npy"), str(tmp_path / "o"), "--gamma-set", "0", host=host)
+        assert r.returncode == 2 and "step factors must be finite and positive" in r.stderr, r.stderr
+    (tmp_path / "z.hdr").write_text("ENVI\nsamples = 2\nlines = 2\nbands = 3\ndata type = 5\n"
+                                    "interleave = bsq\nwavelength = {1, 2}\n")
+    (tmp_path / "z.img").write_bytes(bytes(8 * 12))
+    for host in (False, True):
+        r = unmix(str(tmp_path / "z.hdr"), str(tmp_path / "o"), host=host)
+        assert r.returncode == 2 and "wavelength list length differs" in r.stderr, r.stderr
+    (tmp_path / "z.hdr").write_text("ENVI\nsamples = 2\nlines = 2\nbands = 3\ndata type = 5\ninterleave = bsq\n")
+    for host in (False, True):
+        r = unmix(str(tmp_path / "z.hdr"), str(tmp_path / "o"), host=host)
+        assert r.returncode == 2 and "degenerate input: all pixels are zero" in r.stderr, r.stderr
