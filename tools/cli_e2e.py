@@ -62,6 +62,19 @@ def main():
     for mode in ("device_ingest", "host_normalize"):
         res[mode] = {"process_wall_s": out[mode]["median_s"], "first_call_s": out[mode]["first_s"],
                      "run_iterations_per_s": spec.runs * T / out[mode]["median_s"]}
+    # in-process timing (context and graph warm): tools/cli_bench.cpp
+    exe = os.path.join(d, "cli_bench")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tools", "cli_bench.cpp"), "-L" + os.path.dirname(CLI),
+                    "-larchetype_b200", "-ledaa_cuda", "-Wl,-rpath," + os.path.dirname(CLI), "-o", exe],
+                   check=True)
+    p = subprocess.run([exe, cube, str(spec.endmembers), str(spec.runs), d, str(max(reps, 3))],
+                       capture_output=True, text=True, check=True)
+    lines = [json.loads(l) for l in p.stdout.splitlines()]
+    for mode, key in ((0, "device_ingest"), (1, "host_normalize")):
+        best = min((l for l in lines if l["host_normalize"] == mode), key=lambda l: l["median_ms"])
+        res[key]["in_process_median_ms"] = best["median_ms"]
+        res[key]["in_process_run_iterations_per_s"] = spec.runs * T / (best["median_ms"] / 1e3)
     print(json.dumps(res))
 
 
