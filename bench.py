@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--outer", type=int, default=100, help="T (default: the reference's 100)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--x64", action="store_true",
+                    help="re-normalise the cube in fp64 (as l2_normalize does for a real cube, not "
+                         "fp32-exact): the fp64-X pass kernels, the `unmix` CLI path; not the headline")
     return ap.parse_args()
 
 
@@ -183,7 +186,9 @@ def workload_config(spec, args, runs=None, T=None):
             "bands": spec.bands, "pixels": spec.pixels, "endmembers": spec.endmembers,
             "runs_per_gpu": runs or spec.runs, "outer_iters": T or args.outer,
             "inner_iters": [5, 5], "l2_flush": "256 MB write before every timed step",
-            "parallelism": "ensemble runs sharded over GPUs (weak scaling)"}
+            "parallelism": "ensemble runs sharded over GPUs (weak scaling)",
+            "x_storage": "fp64 (cube re-normalised in fp64: not fp32-exact)" if getattr(args, "x64", False)
+                         else "fp32 (fp32-exact normalised cube)"}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -203,9 +208,13 @@ def main():
     L, N, p, M, T = spec.bands, spec.pixels, spec.endmembers, spec.runs, args.outer
     dev = edaa.Device.get(local)
     stream = torch.cuda.ExternalStream(dev.stream, device=torch.device("cuda", local))
+    if args.x64:
+        x = x.astype(np.float64)
+        x = x / np.sqrt((x * x).sum(axis=0))[None, :]
     x_dev = torch.from_numpy(x).to(f"cuda:{local}")
+    x_img = x if args.x64 else x_dev  # host fp64 upload keeps X in fp64 on the device
     torch.cuda.synchronize()
-    dev.set_image(x_dev)
+    dev.set_image(x_img)
     cfg = edaa.EnsembleConfig(runs=M * world, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
     seeds, gammas = edaa.ensemble_plan(cfg, first=rank * M, count=M)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
@@ -289,7 +298,7 @@ def main():
         e2e = {"value": M * world * T * args.steps / float(dt.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(x.nbytes + 16 * M),
                "d2h_bytes_per_step": int(8 * (2 * p * N + L * p + (T + 1)) + 32 * M)}
-        dev.set_image(x_dev)
+        dev.set_image(x_img)
     if not args.no_e2e and world == 1:
         x_pin = torch.from_numpy(x).pin_memory().numpy()
         ecfg = edaa.EnsembleConfig(runs=M, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
@@ -302,7 +311,7 @@ def main():
         e2e = {"value": M * T * args.steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(x.nbytes + 16 * M),
                "d2h_bytes_per_step": int(8 * (2 * p * N + L * p + (T + 1) * M + 4 * M) + M)}
-        dev.set_image(x_dev)
+        dev.set_image(x_img)
 
     # ---- roofline of the dominant kernel (B-step pass) ----
     peak64 = dev.fp64_peak_tflops()
@@ -310,7 +319,7 @@ def main():
     ms_a, n_a = prof["A"]
     launch_ms = ms_b / max(n_b, 1)
     flops_b = 4.0 * L * N * p * M  # g = XᵀZ and Y = X·B, M runs per launch
-    bytes_b = 4.0 * L * N + 16.0 * p * N * M  # X once + logits read+write (fp64)
+    bytes_b = (8.0 if args.x64 else 4.0) * L * N + 16.0 * p * N * M  # X once + logits read+write (fp64)
     achieved = flops_b / (launch_ms * 1e-3) / 1e12
     peaks = {}
     try:
