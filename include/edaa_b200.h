@@ -117,6 +117,14 @@ EDAA_API int edaa_set_image_device(edaa_ctx* ctx, const float* x, size_t bands, 
  * context's image as L×N fp64 (and its storage width, 4 or 8 bytes). */
 EDAA_API int edaa_ingest_host(edaa_ctx* ctx, const double* x, size_t bands, size_t pixels,
                               size_t* zero_pixels, size_t zero_cap, size_t* n_zero);
+/* The same ingest from an fp32 payload as stored in the file, without the
+ * host widening and reorder: pixel_major = 0 for an L×N band-major image,
+ * 1 for an N×L pixel-major one (an (H, W, L) NPY cube, npy_to_image's pixel
+ * index r·W + c).  Results, zero list and messages are those of
+ * edaa_ingest_host on npy_to_image's fp64 image (fp32 widens exactly); the
+ * upload is half the bytes. */
+EDAA_API int edaa_ingest_host_f32(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels,
+                                  int pixel_major, size_t* zero_pixels, size_t zero_cap, size_t* n_zero);
 EDAA_API int edaa_image_get(edaa_ctx* ctx, double* out, int* xbytes);
 
 /* Batched Algorithm 1 over all runs.  _async only enqueues on edaa_stream();

@@ -56,6 +56,8 @@ SIGNATURES = [
                                         C.c_size_t]),
     ("edaa_ingest_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p,
                                    C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("edaa_ingest_host_f32", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_int,
+                                       C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("edaa_image_get", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]),
     ("edaa_solve_async", C.c_int, [C.c_void_p, C.POINTER(SolveParams)]),
     ("edaa_finish", C.c_int, [C.c_void_p]),

@@ -150,7 +150,17 @@ __global__ void k_pad_copy(const XT* src, size_t ld, XT* dst, int L, int N, int 
 // the result is bitwise the reference's.  Zero pixels are flagged and left as
 // they are; `inexact` is raised if any normalised value is not representable in
 // fp32 (then the solve keeps the fp64 image).
-__global__ void k_ingest(const double* raw, double* xn, int L, int N, int Npad, unsigned long long* bad,
+// Source element (band i, pixel j) of the raw image: band-major L×N (BSQ, the
+// HsiImage layout) or pixel-major N×L (an (H, W, L) NPY cube, npy.cpp:186-207,
+// whose npy_to_image transpose is thereby done here). fp32 sources widen
+// exactly, so every later step sees the reference's fp64 values.
+template <class T, bool PIXEL_MAJOR>
+__device__ __forceinline__ double raw_at(const T* raw, int L, int N, int i, int j) {
+  return static_cast<double>(PIXEL_MAJOR ? raw[static_cast<size_t>(j) * L + i] : raw[static_cast<size_t>(i) * N + j]);
+}
+
+template <class T, bool PIXEL_MAJOR>
+__global__ void k_ingest(const T* raw, double* xn, int L, int N, int Npad, unsigned long long* bad,
                          unsigned char* zero, unsigned int* inexact) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= Npad) return;
@@ -160,7 +170,7 @@ __global__ void k_ingest(const double* raw, double* xn, int L, int N, int Npad, 
   }
   double s = 0.0;
   for (int i = 0; i < L; ++i) {
-    const double v = raw[static_cast<size_t>(i) * N + j];
+    const double v = raw_at<T, PIXEL_MAJOR>(raw, L, N, i, j);
     const unsigned long long idx = static_cast<unsigned long long>(i) * N + j;
     if (!isfinite(v))
       atomicMin(bad + 0, idx);
@@ -173,7 +183,7 @@ __global__ void k_ingest(const double* raw, double* xn, int L, int N, int Npad, 
   zero[j] = z ? 1 : 0;
   bool exact = true;
   for (int i = 0; i < L; ++i) {
-    const double v = raw[static_cast<size_t>(i) * N + j];
+    const double v = raw_at<T, PIXEL_MAJOR>(raw, L, N, i, j);
     const double o = z ? v : __ddiv_rn(v, norm);
     xn[static_cast<size_t>(i) * Npad + j] = o;
     exact &= (static_cast<double>(static_cast<float>(o)) == o);
@@ -941,15 +951,20 @@ int edaa_set_image_device(edaa_ctx* c, const float* x, size_t bands, size_t pixe
   return EDAA_OK;
 }
 
-int edaa_ingest_host(edaa_ctx* c, const double* x, size_t bands, size_t pixels, size_t* zero_pixels,
-                     size_t zero_cap, size_t* n_zero) {
+// Shared by the fp64 and fp32 ingests: upload the raw image as given, then
+// validate + normalise it on the device (k_ingest) into the solver's image.
+}  // extern "C"
+
+template <class T, bool PIXEL_MAJOR>
+static int ingest_impl(edaa_ctx* c, const T* x, size_t bands, size_t pixels, size_t* zero_pixels,
+                       size_t zero_cap, size_t* n_zero) {
   if (!c || !x) return set_err(c, EDAA_ERR_INVALID, "null argument");
   if (bands < 1 || pixels < 1) return set_err(c, EDAA_ERR_INVALID, "image: needs at least one band and one pixel");
   if (pixels > (1u << 30) || bands > (1u << 20)) return set_err(c, EDAA_ERR_UNSUPPORTED, "image too large");
   EDAA_CUDA(c, cudaSetDevice(c->device));
   const int L = static_cast<int>(bands), N = static_cast<int>(pixels);
   const int Npad = (N + edaa::kNP - 1) / edaa::kNP * edaa::kNP;
-  const size_t raw_bytes = bands * pixels * 8, xn_bytes = static_cast<size_t>(L) * Npad * 8;
+  const size_t raw_bytes = bands * pixels * sizeof(T), xn_bytes = static_cast<size_t>(L) * Npad * 8;
   EDAA_CUDA(c, ensure(c->in_raw, raw_bytes));
   EDAA_CUDA(c, ensure(c->in_x, xn_bytes));
   EDAA_CUDA(c, ensure(c->in_flags, static_cast<size_t>(Npad)));
@@ -959,9 +974,9 @@ int edaa_ingest_host(edaa_ctx* c, const double* x, size_t bands, size_t pixels, 
   EDAA_CUDA(c, cudaMemsetAsync(c->in_bad.p, 0xFF, 16, st));
   EDAA_CUDA(c, cudaMemsetAsync(static_cast<char*>(c->in_bad.p) + 16, 0, 8, st));
   unsigned long long* bad = P<unsigned long long>(c->in_bad);
-  k_ingest<<<(Npad + 127) / 128, 128, 0, st>>>(P<double>(c->in_raw), P<double>(c->in_x), L, N, Npad, bad,
-                                               P<unsigned char>(c->in_flags),
-                                               reinterpret_cast<unsigned int*>(bad + 2));
+  k_ingest<T, PIXEL_MAJOR><<<(Npad + 127) / 128, 128, 0, st>>>(
+      P<T>(c->in_raw), P<double>(c->in_x), L, N, Npad, bad, P<unsigned char>(c->in_flags),
+      reinterpret_cast<unsigned int*>(bad + 2));
   EDAA_LAUNCH(c, cudaGetLastError());
   unsigned long long hb[3];
   std::vector<unsigned char> flags(N);
@@ -994,6 +1009,19 @@ int edaa_ingest_host(edaa_ctx* c, const double* x, size_t bands, size_t pixels, 
   d.xbytes = xbytes;
   EDAA_LAUNCH(c, edaa::launch_xnorm(c->X, c->xnorm, d, st));
   return EDAA_OK;
+}
+
+extern "C" {
+
+int edaa_ingest_host(edaa_ctx* c, const double* x, size_t bands, size_t pixels, size_t* zero_pixels,
+                     size_t zero_cap, size_t* n_zero) {
+  return ingest_impl<double, false>(c, x, bands, pixels, zero_pixels, zero_cap, n_zero);
+}
+
+int edaa_ingest_host_f32(edaa_ctx* c, const float* x, size_t bands, size_t pixels, int pixel_major,
+                         size_t* zero_pixels, size_t zero_cap, size_t* n_zero) {
+  return pixel_major ? ingest_impl<float, true>(c, x, bands, pixels, zero_pixels, zero_cap, n_zero)
+                     : ingest_impl<float, false>(c, x, bands, pixels, zero_pixels, zero_cap, n_zero);
 }
 
 int edaa_image_get(edaa_ctx* c, double* out, int* xbytes) {

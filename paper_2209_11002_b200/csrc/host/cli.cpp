@@ -180,14 +180,46 @@ struct UnmixArgs {
 };
 
 int unmix(const UnmixArgs& args, std::ostream& out) {
-  const HsiImage cube = load_cube(args.input);
+  // validate → ℓ2-normalise → all M runs as one batched GPU solve. The image
+  // goes to the device as it is stored and is validated + normalised there
+  // (edaa_ingest_host[_f32]: the reference's bits, its messages in its
+  // order): an fp32 .npy payload is uploaded as fp32 without the host
+  // widening / (H, W, L) reorder; other inputs as the loaded fp64 image.
+  // ARCHETYPE_HOST_NORMALIZE=1 takes the reference's host fp64 route instead.
+  const char* host_env = std::getenv("ARCHETYPE_HOST_NORMALIZE");
+  const bool host_route = host_env && *host_env && std::string(host_env) != "0";
+  std::optional<detail::NpyPayload> payload;
+  HsiImage cube;
+  if (!host_route && ends_with_ci(args.input, ".npy")) {
+    payload = detail::read_npy_payload(args.input);
+    const std::size_t dims = payload->shape.size();
+    if (payload->dtype != NpyDtype::f4 || (dims != 2 && dims != 3)) {
+      NpyArray widened;  // npy_to_image raises the reference's rank message
+      widened.shape = payload->shape;
+      widened.dtype = payload->dtype;
+      widened.values = payload->dtype == NpyDtype::f8
+                           ? std::move(payload->f64)
+                           : std::vector<double>(payload->f32.begin(), payload->f32.end());
+      cube = npy_to_image(widened);
+      payload.reset();
+    }
+  } else {
+    cube = load_cube(args.input);
+  }
 
   RunReport report;
   report.version = kVersion;
   report.input_path = args.input;
-  report.bands = cube.bands();
-  report.pixels = cube.pixels();
-  report.spatial = cube.spatial;
+  if (payload) {  // (bands, pixels) or (H, W, bands), as npy_to_image reads them
+    const auto& sh = payload->shape;
+    report.bands = sh.size() == 2 ? sh[0] : sh[2];
+    report.pixels = sh.size() == 2 ? sh[1] : sh[0] * sh[1];
+    if (sh.size() == 3) report.spatial = Shape2d{sh[0], sh[1]};
+  } else {
+    report.bands = cube.bands();
+    report.pixels = cube.pixels();
+    report.spatial = cube.spatial;
+  }
   EnsembleConfig& cfg = report.config;
   cfg.runs = args.runs;
   cfg.base_seed = args.seed;
@@ -198,16 +230,15 @@ int unmix(const UnmixArgs& args, std::ostream& out) {
   cfg.solver.inner_iters_a = args.inner;
   cfg.solver.inner_iters_b = args.inner;
 
-  // validate → ℓ2-normalise → all M runs as one batched GPU solve. The
-  // normalisation runs in the device ingest (the reference's bits and
-  // messages); ARCHETYPE_HOST_NORMALIZE=1 takes the host fp64 route instead.
   std::pair<RunResult, SelectionReport> solved;
-  const char* host_norm = std::getenv("ARCHETYPE_HOST_NORMALIZE");
-  if (host_norm && *host_norm && std::string(host_norm) != "0") {
+  if (host_route) {
     cube.validate();
     const NormalizeResult norm = l2_normalize(cube);
     report.zero_pixels = norm.zero_pixels.size();
     solved = run_ensemble(norm.image, cfg);
+  } else if (payload) {
+    solved = detail::run_ensemble_raw_f32(payload->f32.data(), report.bands, report.pixels,
+                                          payload->shape.size() == 3, cfg, report.zero_pixels);
   } else {
     solved = detail::run_ensemble_raw(cube, cfg, report.zero_pixels);
   }

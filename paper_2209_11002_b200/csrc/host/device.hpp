@@ -10,6 +10,7 @@
 #include "archetype/error.hpp"
 #include "archetype/image.hpp"
 #include "archetype/matrix.hpp"
+#include "archetype/npy.hpp"
 #include "archetype/solver.hpp"
 #include "edaa_b200.h"
 
@@ -37,5 +38,21 @@ void upload_image(Device& d, const Matrix& x);
 /// receives NormalizeResult::zero_pixels.size(). The CLI's `unmix` path.
 std::pair<RunResult, SelectionReport> run_ensemble_raw(const HsiImage& raw, const EnsembleConfig& config,
                                                        std::size_t& zero_pixels);
+/// The same from an fp32 NPY payload as stored (L×N band-major, or the N×L
+/// pixel-major payload of an (H, W, L) cube): no host widening or reorder,
+/// half the upload (edaa_ingest_host_f32).
+std::pair<RunResult, SelectionReport> run_ensemble_raw_f32(const float* x, std::size_t bands, std::size_t pixels,
+                                                           bool pixel_major, const EnsembleConfig& config,
+                                                           std::size_t& zero_pixels);
+
+/// NPY payload without widening: shape, dtype and the raw little-endian bytes.
+struct NpyPayload {
+  std::vector<std::size_t> shape;
+  NpyDtype dtype = NpyDtype::f8;
+  std::vector<float> f32;    // when dtype == f4
+  std::vector<double> f64;   // when dtype == f8
+};
+/// read_npy's parsing and messages, keeping an f4 payload in fp32.
+NpyPayload read_npy_payload(const std::string& path);
 
 }  // namespace archetype::detail

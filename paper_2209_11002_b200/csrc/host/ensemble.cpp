@@ -247,19 +247,21 @@ static void check_shape(const HsiImage& raw) {
     throw Error("image: wavelength list length differs from band count");
 }
 
-std::pair<RunResult, SelectionReport> run_ensemble_raw(const HsiImage& raw, const EnsembleConfig& config,
-                                                       std::size_t& zero_pixels) {
-  if (raw.bands() < 1 || raw.pixels() < 1) raw.validate();  // the reference's size message
-  // Value checks + ℓ2 normalisation on the device (edaa_ingest_host) in the
-  // reference's order of messages: a bad value, then the shape checks, then
-  // "degenerate input" — all before the config is looked at, as `unmix`
-  // validates and normalises the image before run_ensemble (cli.cpp:75-78).
-  const auto ingest = [&raw](Device& d) {
+// Ingest (validate + ℓ2-normalise on the device) then the batched solve, in
+// the reference's order of messages: a bad value, then the shape checks, then
+// "degenerate input" — all before the config is looked at, as `unmix`
+// validates and normalises the image before run_ensemble (cli.cpp:75-78).
+// `upload` runs edaa_ingest_host[_f32] on one device and returns its status.
+static std::pair<RunResult, SelectionReport> ingest_and_solve(const std::function<int(Device&, std::size_t&)>& upload,
+                                                              const std::function<void()>& shape_check,
+                                                              std::size_t l, std::size_t n,
+                                                              const EnsembleConfig& config,
+                                                              std::size_t& zero_pixels) {
+  const auto ingest = [&](Device& d) {
     std::size_t nz = 0;
-    if (edaa_ingest_host(d.ctx, raw.data.values().data(), raw.bands(), raw.pixels(), nullptr, 0, &nz) !=
-        EDAA_OK) {
+    if (upload(d, nz) != EDAA_OK) {
       const std::string what = edaa_last_error(d.ctx);
-      if (what.rfind("degenerate", 0) == 0) check_shape(raw);
+      if (what.rfind("degenerate", 0) == 0) shape_check();
       throw Error(what);
     }
     return nz;
@@ -269,11 +271,35 @@ std::pair<RunResult, SelectionReport> run_ensemble_raw(const HsiImage& raw, cons
     std::lock_guard<std::mutex> lock(first.mu);
     zero_pixels = ingest(first);
   }
-  check_shape(raw);
+  shape_check();
   config.validate();
   // Device 0 already holds the normalised image; further devices ingest their own copy.
-  return ensemble_on_devices([&](Device& d) { if (&d != &first) ingest(d); }, raw.bands(), raw.pixels(),
-                             config);
+  return ensemble_on_devices([&](Device& d) { if (&d != &first) ingest(d); }, l, n, config);
+}
+
+std::pair<RunResult, SelectionReport> run_ensemble_raw(const HsiImage& raw, const EnsembleConfig& config,
+                                                       std::size_t& zero_pixels) {
+  if (raw.bands() < 1 || raw.pixels() < 1) raw.validate();  // the reference's size message
+  return ingest_and_solve(
+      [&raw](Device& d, std::size_t& nz) {
+        return edaa_ingest_host(d.ctx, raw.data.values().data(), raw.bands(), raw.pixels(), nullptr, 0, &nz);
+      },
+      [&raw] { check_shape(raw); }, raw.bands(), raw.pixels(), config, zero_pixels);
+}
+
+std::pair<RunResult, SelectionReport> run_ensemble_raw_f32(const float* x, std::size_t bands, std::size_t pixels,
+                                                           bool pixel_major, const EnsembleConfig& config,
+                                                           std::size_t& zero_pixels) {
+  if (bands < 1 || pixels < 1) {
+    HsiImage empty;
+    empty.data = Matrix(bands, pixels);
+    empty.validate();
+  }
+  return ingest_and_solve(
+      [&](Device& d, std::size_t& nz) {
+        return edaa_ingest_host_f32(d.ctx, x, bands, pixels, pixel_major ? 1 : 0, nullptr, 0, &nz);
+      },
+      [] {}, bands, pixels, config, zero_pixels);  // an NPY cube has a consistent shape, no wavelengths
 }
 
 }  // namespace detail

@@ -14,6 +14,7 @@
 #include <string_view>
 
 #include "archetype/error.hpp"
+#include "device.hpp"
 
 namespace archetype {
 
@@ -97,7 +98,9 @@ std::size_t NpyArray::element_count() const {
   return n;
 }
 
-NpyArray read_npy(const std::string& path) {
+namespace detail {
+
+NpyPayload read_npy_payload(const std::string& path) {
   std::ifstream file(path, std::ios::binary);
   if (!file) npy_error(path, "cannot open file");
 
@@ -122,7 +125,7 @@ NpyArray read_npy(const std::string& path) {
 
   const HeaderDict dict{header, path};
   const std::string descr = dict.quoted_value("descr");
-  NpyArray array;
+  NpyPayload array;
   if (descr == "<f4") {
     array.dtype = NpyDtype::f4;
   } else if (descr == "<f8") {
@@ -134,19 +137,32 @@ NpyArray read_npy(const std::string& path) {
   array.shape = dict.tuple_value("shape");
   if (array.shape.empty()) npy_error(path, "zero-dimensional array");
 
-  const std::size_t count = array.element_count();
-  array.values.resize(count);
-  if (array.dtype == NpyDtype::f8) {
-    const auto want = static_cast<std::streamsize>(count * sizeof(double));
-    file.read(reinterpret_cast<char*>(array.values.data()), want);
+  std::size_t count = 1;
+  for (const std::size_t d : array.shape) count *= d;
+  const auto fill = [&](auto& buf) {
+    buf.resize(count);
+    const auto want = static_cast<std::streamsize>(count * sizeof(buf[0]));
+    file.read(reinterpret_cast<char*>(buf.data()), want);
     if (file.gcount() != want) npy_error(path, "truncated data section");
-  } else {
-    std::vector<float> narrow(count);
-    const auto want = static_cast<std::streamsize>(count * sizeof(float));
-    file.read(reinterpret_cast<char*>(narrow.data()), want);
-    if (file.gcount() != want) npy_error(path, "truncated data section");
-    for (std::size_t i = 0; i < count; ++i) array.values[i] = narrow[i];
-  }
+  };
+  if (array.dtype == NpyDtype::f8)
+    fill(array.f64);
+  else
+    fill(array.f32);
+  return array;
+}
+
+}  // namespace detail
+
+NpyArray read_npy(const std::string& path) {
+  detail::NpyPayload raw = detail::read_npy_payload(path);
+  NpyArray array;
+  array.shape = std::move(raw.shape);
+  array.dtype = raw.dtype;
+  if (raw.dtype == NpyDtype::f8)
+    array.values = std::move(raw.f64);
+  else
+    array.values.assign(raw.f32.begin(), raw.f32.end());  // exact widening
   return array;
 }
 

@@ -282,6 +282,22 @@ class Device:
         self.L, self.N = L, N
         return [int(v) for v in zp[:nz.value]]
 
+    def ingest_f32(self, x, pixel_major: bool = False) -> List[int]:
+        """The same from an fp32 payload as stored: x is L×N (band-major) or,
+        with pixel_major, the N×L payload of an (H, W, L) cube
+        (edaa_ingest_host_f32).  Returns the zero pixels."""
+        xr = np.ascontiguousarray(x, dtype=np.float32)
+        if xr.ndim != 2:
+            raise EdaaError("image: needs at least one band and one pixel")
+        N, L = xr.shape if pixel_major else xr.shape[::-1]
+        zp = np.zeros(max(N, 1), dtype=np.uint64)
+        nz = C.c_size_t()
+        self._check(self.lib.edaa_ingest_host_f32(self.h, xr.ctypes.data_as(C.c_void_p), L, N,
+                                                  1 if pixel_major else 0, zp.ctypes.data_as(C.c_void_p),
+                                                  zp.size, C.byref(nz)))
+        self.L, self.N = L, N
+        return [int(v) for v in zp[:nz.value]]
+
     def image(self):
         """(the device image as L×N fp64, its storage width in bytes: 4 or 8)."""
         out = np.zeros((self.L, self.N))

@@ -117,7 +117,8 @@ def test_reference_acceptance_gate_passes_on_gpu():
 
 
 @pytest.mark.gpu
-def test_cli_device_ingest_equals_host_normalisation(tmp_path):
+@pytest.mark.parametrize("dtype", ["<f8", "<f4"])
+def test_cli_device_ingest_equals_host_normalisation(tmp_path, dtype):
     """`unmix` normalises through the device ingest; ARCHETYPE_HOST_NORMALIZE=1
     takes the reference's host fp64 route. The bundles are identical (but for
     the measured wall_ms), and the error messages come in the reference's
@@ -135,6 +136,7 @@ def test_cli_device_ingest_equals_host_normalisation(tmp_path):
     rng = np.random.default_rng(11)
     x = rng.random((5, 7, 19)) ** 2 + 0.01   # (H, W, L): not fp32-exact after normalising
     x[2, 3, :] = 0.0                          # one zero pixel, left unnormalised
+    x = x.astype(dtype)                       # <f4: the fp32 payload ingest (no host widening)
     np.save(tmp_path / "cube.npy", x)
     a = unmix(str(tmp_path / "cube.npy"), str(tmp_path / "dev"))
     b = unmix(str(tmp_path / "cube.npy"), str(tmp_path / "host"), host=True)

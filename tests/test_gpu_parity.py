@@ -333,6 +333,33 @@ def test_device_ingest_is_bitwise_the_reference_l2_normalize():
     assert dev().image()[1] == 8  # not fp32-exact: the fp64 image path
 
 
+def test_fp32_payload_ingest_equals_the_widened_fp64_ingest():
+    """edaa_ingest_host_f32 (the `unmix` route for fp32 .npy cubes): band-major
+    and pixel-major (H, W, L) payloads give bitwise the image, zero list and
+    first-offending-element message of the fp64 ingest of npy_to_image's cube."""
+    rng = np.random.default_rng(21)
+    cube = (rng.random((9, 13, 31)) ** 2).astype(np.float32)   # (H, W, L)
+    cube[4, 7, :] = 0.0
+    bsq = cube.reshape(-1, 31).T.astype(np.float64)             # npy_to_image: L×(H·W), pixel r·W + c
+    want_zero = dev().ingest(bsq)
+    want, wbytes = dev().image()
+    assert want_zero == [4 * 13 + 7]
+    got_zero = dev().ingest_f32(cube.reshape(-1, 31), pixel_major=True)
+    got, gbytes = dev().image()
+    assert got_zero == want_zero and gbytes == wbytes and np.array_equal(got, want)
+    got_zero = dev().ingest_f32(np.ascontiguousarray(bsq.astype(np.float32)))
+    got, gbytes = dev().image()
+    assert got_zero == want_zero and gbytes == wbytes and np.array_equal(got, want)
+    bad = cube.copy()
+    bad[0, 5, 3] = -1.0      # BSQ flat index 3·N + 5
+    bad[2, 0, 1] = np.nan    # BSQ flat index 1·N + 26: earlier in the reference's scan
+    with pytest.raises(edaa.EdaaError, match="non-finite reflectance"):
+        dev().ingest_f32(bad.reshape(-1, 31), pixel_major=True)
+    bad[2, 0, 1] = 1.0
+    with pytest.raises(edaa.EdaaError, match="negative reflectance"):
+        dev().ingest_f32(bad.reshape(-1, 31), pixel_major=True)
+
+
 def test_device_ingest_errors_and_fp32_detection():
     x = np.ones((4, 9))
     y = x.copy(); y[1, 2] = -1.0; y[3, 0] = np.nan
