@@ -311,3 +311,21 @@ def test_cli_host_cases_pass():
     r = subprocess.run([CLI_TEST, "host"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+@pytest.mark.parametrize("p", [3, 10])
+def test_evaluate_tie_breaking_matches_reference(tmp_path, p):
+    """Duplicate spectra make several matchings optimal: the exhaustive search
+    (p ≤ 8, first strict minimum in lexicographic order) and the Hungarian
+    method (p > 8, column scan order) must pick the reference's."""
+    rng = np.random.default_rng(40 + p)
+    gt_e = rng.random((12, p)) + 0.1
+    gt_e[:, 1] = gt_e[:, 0]
+    gt_e[:, p - 1] = gt_e[:, 0]
+    gt_a = rng.dirichlet(np.ones(p), size=50).T
+    est_e = np.repeat(gt_e[:, :1], p, axis=1)        # every pairing of the copies costs the same
+    est_e[:, 2:p - 1] = gt_e[:, 2:p - 1][:, ::-1]
+    _write_est(str(tmp_path / "est"), est_e, gt_a[::-1])
+    save(tmp_path / "gt_a.npy", gt_a)
+    save(tmp_path / "gt_e.npy", gt_e)
+    same("evaluate", tmp_path / "est", tmp_path / "gt_e.npy", tmp_path / "gt_a.npy")
