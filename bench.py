@@ -125,17 +125,32 @@ def scene(cfg_name):
 
 
 # ----------------------------------------------------------------------------- reference arm
+# The reference's cost is ~62·L·N·p flops per run-iteration, linear in N
+# (SURVEY §3.2); above this L·N·p the CPU sample runs on the first
+# CPU_SAMPLE_LNP/(L·p) pixels and its time is scaled by N/N' (cfg2-cfg4: a
+# full cfg4 run-iteration is ~2 min per core, and 16 concurrent runs need
+# ~100 GB of host temporaries).
+CPU_SAMPLE_LNP = 2.0e7
+
+
+def cpu_sample_pixels(spec):
+    n = int(CPU_SAMPLE_LNP // (spec.bands * spec.endmembers))
+    return spec.pixels if spec.bands * spec.pixels * spec.endmembers <= CPU_SAMPLE_LNP else max(n, 64)
+
+
 def cpu_reference_sample(x, spec, T, runs=None, workers=None):
-    """Reference run_ensemble on the host cores: returns (seconds, run-iters done, kind, cores)."""
+    """Reference run_ensemble on the host cores: returns (seconds scaled to the
+    full N, run-iters done, kind, cores)."""
     from oracle import Oracle, available_kinds
     kind = "reference" if "reference" in available_kinds() else "port"
     orc = Oracle(kind)
     cores = workers or os.cpu_count() or 1
     runs = runs or cores
-    xd = x.astype(np.float64)
+    n = cpu_sample_pixels(spec)
+    xd = np.ascontiguousarray(x[:, :n], dtype=np.float64)
     t0 = time.perf_counter()
     orc.run_ensemble(xd, spec.endmembers, M=runs, T=T, workers=cores)
-    return time.perf_counter() - t0, runs * T, kind, cores
+    return (time.perf_counter() - t0) * (spec.pixels / n), runs * T, kind, cores
 
 
 def cpu_baseline(x, spec):
@@ -146,7 +161,13 @@ def cpu_baseline(x, spec):
     value = cores * 3 / max(t4 - t1, 1e-9)
     return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": "%s shape, M=%d concurrent runs (one per core), T=4 minus T=1 "
-                      "(%.1f s + %.1f s wall)" % (spec.name, cores, t4, t1)}
+                      "(%.1f s + %.1f s wall)%s" % (spec.name, cores, t4, t1, sample_note(spec))}
+
+
+def sample_note(spec):
+    n = cpu_sample_pixels(spec)
+    return "" if n == spec.pixels else (", on the first %d of %d pixels, time scaled by N/N' "
+                                        "(reference cost is linear in N)" % (n, spec.pixels))
 
 
 def run_reference_arm(args):
@@ -172,7 +193,8 @@ def run_reference_arm(args):
         "data": "synthetic", "config": workload_config(spec, args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": "%s shape, M=%d runs (one per core) x T=%d per step, "
-                                   "run_ensemble with %d workers" % (spec.name, cores, T, cores)},
+                                   "run_ensemble with %d workers%s" % (spec.name, cores, T, cores,
+                                                                      sample_note(spec))},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
