@@ -175,9 +175,7 @@ EDAA_API int edaa_set_shard_emulation(edaa_ctx* ctx, int world);
 
 /* Order of the pass kernels' (pixel slice, run chunk) work items (no reference
  * counterpart: a scheduling knob of this implementation).  0 = auto (chunk-major
- * when X fits in L2, else interleaved when the items divide evenly over the
- * CTAs, else slice-major), 1 = chunk-major, 2 = slice-major, 3 = interleaved
- * (CTA b takes slice-major items b, b+G, b+2G, …; slice-major if uneven).  The
+ * when X fits in L2, else slice-major), 1 = chunk-major, 2 = slice-major.  The
  * per-(slice, chunk) partials, and so every result, are bitwise the same for
  * all orders; only the speed differs. */
 EDAA_API int edaa_set_pass_order(edaa_ctx* ctx, int order);

@@ -362,15 +362,10 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.pdl = (d.NCH * (d.sl1 - d.sl0) < c->num_sms) ? 1 : 0;
   // Chunk-major pass items when X is comfortably L2-resident (126 MB L2 on B200,
   // shared with the slice partials), unless edaa_set_pass_order picks one.
-  // Larger images: interleaved items when every CTA gets the same count
-  // (nslices = #SMs for large N), else slice-major.
-  const bool even = (d.NCH * (d.sl1 - d.sl0)) % d.ncta == 0;
-  if (c->pass_order >= 1 && c->pass_order <= 3)
-    d.cmajor = (c->pass_order == 1) ? 1 : (c->pass_order == 3 && even) ? 2 : 0;
-  else if (static_cast<size_t>(d.Lpad) * d.Npad * d.xbytes <= (size_t(96) << 20))
-    d.cmajor = 1;
+  if (c->pass_order == 1 || c->pass_order == 2)
+    d.cmajor = (c->pass_order == 1) ? 1 : 0;
   else
-    d.cmajor = even ? 2 : 0;
+    d.cmajor = (static_cast<size_t>(d.Lpad) * d.Npad * d.xbytes <= (size_t(96) << 20)) ? 1 : 0;
   // X ring depth and W chunk buffers, the deepest that fits shared memory.
   static const int kRing[][2] = {{4, 2}, {3, 2}, {3, 1}, {2, 2}, {2, 1}};
   for (const auto& rw : kRing) {
@@ -1104,7 +1099,7 @@ int edaa_finish(edaa_ctx* c) {
 
 int edaa_set_pass_order(edaa_ctx* c, int order) {
   if (!c) return EDAA_ERR_INVALID;
-  if (order < 0 || order > 3) return set_err(c, EDAA_ERR_INVALID, "pass order must be 0 (auto), 1, 2 or 3");
+  if (order < 0 || order > 2) return set_err(c, EDAA_ERR_INVALID, "pass order must be 0 (auto), 1 or 2");
   c->pass_order = order;
   return EDAA_OK;
 }

@@ -283,23 +283,12 @@ __host__ __device__ __forceinline__ int slice_tile(const Dims& d, int s) {
 //     re-read from L2 once per chunk (chosen when X fits in L2);
 //   slice-major: k = (slice − sl0)·NCH + chunk — consecutive items re-read the
 //     same X slice (large images).
-//   interleaved (cmajor == 2, X larger than L2, K a multiple of the grid): CTA b's
-//     j-th item is slice-major item j·G + b, so at any moment the G CTAs work on
-//     G consecutive slice-major items — ~G/NCH slices, every chunk of each —
-//     and a slice's X tiles, read from HBM by the first of its CTAs, are L2
-//     hits for the others. (Plain slice-major gives each CTA one whole slice:
-//     all of X is in flight at once and re-read from HBM once per chunk.)
-// Every order computes the same per-(slice, chunk) partials: results are bitwise equal.
-__host__ __device__ __forceinline__ int item_phys(const Dims& d, int k) {
-  if (d.cmajor != 2) return k;
-  const int per = d.NCH * (d.sl1 - d.sl0) / d.ncta;  // items per CTA
-  return (k % per) * d.ncta + k / per;
-}
+// Either order computes the same per-(slice, chunk) partials: results are bitwise equal.
 __host__ __device__ __forceinline__ int item_slice(const Dims& d, int k) {
-  return d.cmajor == 1 ? d.sl0 + k % (d.sl1 - d.sl0) : d.sl0 + item_phys(d, k) / d.NCH;
+  return d.cmajor ? d.sl0 + k % (d.sl1 - d.sl0) : d.sl0 + k / d.NCH;
 }
 __host__ __device__ __forceinline__ int item_chunk(const Dims& d, int k) {
-  return d.cmajor == 1 ? k / (d.sl1 - d.sl0) : item_phys(d, k) % d.NCH;
+  return d.cmajor ? k / (d.sl1 - d.sl0) : k % d.NCH;
 }
 __device__ __forceinline__ void cursor_set(Cursor& c, const Dims& d, const int* slt, int item) {
   c.item = item;
@@ -311,10 +300,7 @@ __device__ __forceinline__ void cursor_set(Cursor& c, const Dims& d, const int* 
 __device__ __forceinline__ void cursor_next(Cursor& c, const Dims& d, const int* slt) {
   if (++c.tile != c.tend) return;
   ++c.item;
-  if (d.cmajor == 2) {
-    c.slice = item_slice(d, c.item);
-    c.chunk = item_chunk(d, c.item);
-  } else if (d.cmajor) {  // the next slice of the same chunk, then the next chunk
+  if (d.cmajor) {  // the next slice of the same chunk, then the next chunk
     if (++c.slice == d.sl1) {
       c.slice = d.sl0;
       ++c.chunk;
@@ -520,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           bar_sync(bars::kMma, kGroup);
           // the next item with a different chunk (chunk-major: usually none in this CTA)
           int nx = p1c.item + 1;
-          if (d.cmajor == 1) nx = (item_chunk(d, nx) == chunk) ? (chunk + 1) * (d.sl1 - d.sl0) : nx;
+          if (d.cmajor) nx = (item_chunk(d, nx) == chunk) ? (chunk + 1) * (d.sl1 - d.sl0) : nx;
           if (nx < item_end && item_chunk(d, nx) != chunk) w_fetch(item_chunk(d, nx), wcur ^ 1);
         } else {  // one buffer: restage in place once every MMA warp is past its previous P1
           if (wchunk >= 0) {
