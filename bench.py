@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--outer", type=int, default=100, help="T (default: the reference's 100)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pass-order", type=int, default=0,
+                    help="dev: pass item order (0 auto, 1 chunk-major, 2 slice-major, 3 interleaved)")
     ap.add_argument("--x64", action="store_true",
                     help="re-normalise the cube in fp64 (as l2_normalize does for a real cube, not "
                          "fp32-exact): the fp64-X pass kernels, the `unmix` CLI path; not the headline")
@@ -229,6 +231,8 @@ def main():
     spec, x = scene(args.config)
     L, N, p, M, T = spec.bands, spec.pixels, spec.endmembers, spec.runs, args.outer
     dev = edaa.Device.get(local)
+    if args.pass_order:
+        dev.set_pass_order(args.pass_order)
     stream = torch.cuda.ExternalStream(dev.stream, device=torch.device("cuda", local))
     if args.x64:
         x = x.astype(np.float64)

@@ -175,7 +175,10 @@ EDAA_API int edaa_set_shard_emulation(edaa_ctx* ctx, int world);
 
 /* Order of the pass kernels' (pixel slice, run chunk) work items (no reference
  * counterpart: a scheduling knob of this implementation).  0 = auto (chunk-major
- * when X fits in L2, else slice-major), 1 = chunk-major, 2 = slice-major.  The
+ * when X fits in L2, else slice-major), 1 = chunk-major, 2 = slice-major,
+ * 3 = slice-major interleaved over the CTAs (CTA b takes items b, b+G, …, so
+ * X slices are shared in L2: ~1/3 of the HBM traffic on images far larger
+ * than L2, at about the same speed; plain slice-major if uneven).  The
  * per-(slice, chunk) partials, and so every result, are bitwise the same for
  * all orders; only the speed differs. */
 EDAA_API int edaa_set_pass_order(edaa_ctx* ctx, int order);

@@ -64,6 +64,7 @@ struct Dims {
   int sl0, sl1;  // pixel slices this device owns (pixel sharding; 0..nslices otherwise)
   int pdl;       // programmatic dependent launch for the schedule's kernels (small grids only)
   int cmajor;    // pass item order: 1 chunk-major (X fits in L2), 0 slice-major (edaa_pass.cuh)
+  int ilv;       // slice-major items interleaved over the CTAs (A/B passes, separate instantiation)
 };
 
 struct PassArgs {

@@ -312,6 +312,53 @@ __device__ __forceinline__ void cursor_next(Cursor& c, const Dims& d, const int*
   c.tile = c.tstart = slt[c.slice];
   c.tend = slt[c.slice + 1];
 }
+
+// Interleaved slice-major items (large images, Dims::ilv, the ILV instantiation
+// of the A/B passes): CTA b's j-th item is slice-major item j·G + b, so the G
+// CTAs always work on G consecutive items (~G/NCH slices, every chunk of each)
+// and an X slice read from HBM by its first CTA is an L2 hit for the others —
+// with one slice per CTA, plain slice-major keeps all of X in flight and
+// re-reads it from HBM once per chunk. Same partials, bitwise the same results.
+// The other instantiations (ILV = false) are the code above, unchanged.
+template <bool ILV>
+__device__ __forceinline__ int item_slice_t(const Dims& d, int k) {
+  if constexpr (ILV) {
+    const int per = d.NCH * (d.sl1 - d.sl0) / d.ncta;
+    return d.sl0 + ((k % per) * d.ncta + k / per) / d.NCH;
+  } else {
+    return item_slice(d, k);
+  }
+}
+template <bool ILV>
+__device__ __forceinline__ int item_chunk_t(const Dims& d, int k) {
+  if constexpr (ILV) {
+    const int per = d.NCH * (d.sl1 - d.sl0) / d.ncta;
+    return ((k % per) * d.ncta + k / per) % d.NCH;
+  } else {
+    return item_chunk(d, k);
+  }
+}
+template <bool ILV>
+__device__ __forceinline__ void cursor_set_t(Cursor& c, const Dims& d, const int* slt, int item) {
+  if constexpr (ILV) {
+    c.item = item;
+    c.slice = item_slice_t<true>(d, item);
+    c.chunk = item_chunk_t<true>(d, item);
+    c.tile = c.tstart = slt[c.slice];
+    c.tend = slt[c.slice + 1];
+  } else {
+    cursor_set(c, d, slt, item);
+  }
+}
+template <bool ILV>
+__device__ __forceinline__ void cursor_next_t(Cursor& c, const Dims& d, const int* slt) {
+  if constexpr (ILV) {
+    if (++c.tile != c.tend) return;
+    cursor_set_t<true>(c, d, slt, c.item + 1);
+  } else {
+    cursor_next(c, d, slt);
+  }
+}
 // Position in a ring of n slots walked one step at a time (slot = i % n, phase = (i / n) & 1).
 struct Ring {
   int slot, phase;
@@ -340,7 +387,7 @@ __device__ __forceinline__ ChunkInfo chunk_info(const Dims& d, int chunk) {
 // CTF: DMMA column tiles computed per chunk — kMaxCT, or 1 when the whole batch
 // fits one 8-column tile (a single run with p ≤ 8: cfg0, the pixel-sharded run),
 // which skips the DMMAs of the empty tiles (their w is 0, their partials stay 0).
-template <int MODE, int PT, int RTW, class XT, int CTF>
+template <int MODE, int PT, int RTW, class XT, int CTF, bool ILV = false>
 __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(16) unsigned char smem[];
   const long long t_kernel0 = pa.kprof ? clock64() : 0;
@@ -380,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   const int item_end = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * K) / gridDim.x);
   int ntile = 0;
   for (int k = item_begin; k < item_end; ++k) {
-    const int s = item_slice(d, k);
+    const int s = item_slice_t<ILV>(d, k);
     ntile += slice_tile(d, s + 1) - slice_tile(d, s);
   }  // once per CTA
   if (ntile == 0) return;
@@ -432,9 +479,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     const int my_x = (nRTx - gwarp + 7) / 8;  // of which X rows (the rest: one pseudo tile)
     const bool my_pseudo = my_rt > my_x;
     Cursor xc, p1c, p3c;
-    cursor_set(xc, d, slt, item_begin);
-    cursor_set(p1c, d, slt, item_begin);
-    cursor_set(p3c, d, slt, item_begin);
+    cursor_set_t<ILV>(xc, d, slt, item_begin);
+    cursor_set_t<ILV>(p1c, d, slt, item_begin);
+    cursor_set_t<ILV>(p3c, d, slt, item_begin);
     // W chunk double buffer: ws(wcur) holds chunk wchunk; the next item's chunk is
     // prefetched by cp.async into the other buffer while the current one is in use.
     int wcur = 0, wchunk = -1;
@@ -477,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
                         xc.tile * kNP + h * 16, bx * brows, full + b);
       }
       ldr.next(nbuf);
-      cursor_next(xc, d, slt);
+      cursor_next_t<ILV>(xc, d, slt);
     };
     auto x_wait = [&]() {  // the next tile for P1; returns its slot
       const int b = xwr.slot;
@@ -506,8 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           bar_sync(bars::kMma, kGroup);
           // the next item with a different chunk (chunk-major: usually none in this CTA)
           int nx = p1c.item + 1;
-          if (d.cmajor) nx = (item_chunk(d, nx) == chunk) ? (chunk + 1) * (d.sl1 - d.sl0) : nx;
-          if (nx < item_end && item_chunk(d, nx) != chunk) w_fetch(item_chunk(d, nx), wcur ^ 1);
+          if (d.cmajor) nx = (item_chunk_t<ILV>(d, nx) == chunk) ? (chunk + 1) * (d.sl1 - d.sl0) : nx;
+          if (nx < item_end && item_chunk_t<ILV>(d, nx) != chunk) w_fetch(item_chunk_t<ILV>(d, nx), wcur ^ 1);
         } else {  // one buffer: restage in place once every MMA warp is past its previous P1
           if (wchunk >= 0) {
             bar_sync(bars::kMma, kGroup);
@@ -553,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
             make_double2(c1[ct][0], c1[ct][1]);
     };
 
-    if (MODE != kModeInit && !(pa.dbg & 65)) w_fetch(item_chunk(d, item_begin), 0);  // the first chunk (waited in P1(0))
+    if (MODE != kModeInit && !(pa.dbg & 65)) w_fetch(item_chunk_t<ILV>(d, item_begin), 0);  // the first chunk (waited in P1(0))
     for (int f = 0; f < nbuf - 1 && f < ntile; ++f) load_next_x(f);  // X(0 .. nbuf−2) in flight
     {
       const int xb0 = x_wait();
@@ -561,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       phase1(0, xb0);
     }
     if (pa.kprof && gtid == 0) atomicAdd(pa.kprof + 24 + 3 * MODE, static_cast<unsigned long long>(clock64() - t_kernel0));
-    cursor_next(p1c, d, slt);
+    cursor_next_t<ILV>(p1c, d, slt);
     s_arrive(0);
     // P1(i+1) overlaps the update of tile i (measured faster for both pass kinds than
     // the serial order P3(i) → P1(i+1), EDAA_DBG=1024, which keeps the scalar fp64
@@ -580,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
           phase1(it + 1, xb);
           EDAA_TSTOP(1);
         }
-        cursor_next(p1c, d, slt);
+        cursor_next_t<ILV>(p1c, d, slt);
         s_arrive(it + 1);
       }
     };
@@ -657,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
       const long long tr_ = (pa.kprof && lane == 0 && gwarp == 0) ? clock64() : 0;
       x_release();  // this warp is done with X(i) (P1(i) and P3(i))
       warp_arrive(sfree + (it & 1));  // … and with S(i)/w(i)
-      cursor_next(p3c, d, slt);
+      cursor_next_t<ILV>(p3c, d, slt);
       if (pa.kprof && lane == 0 && gwarp == 0)
         atomicAdd(pa.kprof + 53 + 2 * MODE, static_cast<unsigned long long>(clock64() - tr_));
       if (serial) next_p1(it);
@@ -670,8 +717,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   } else {
     // ========================== update group ==========================
     Cursor sc, p2c;
-    cursor_set(sc, d, slt, item_begin);
-    cursor_set(p2c, d, slt, item_begin);
+    cursor_set_t<ILV>(sc, d, slt, item_begin);
+    cursor_set_t<ILV>(p2c, d, slt, item_begin);
     int cchunk = -1;
     int stl = 0, stu = 0;  // state-tile ring (3 slots): next load, current use
     auto next_state = [&](int f) {  // one commit group per call (empty past the end)
@@ -679,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         const ChunkInfo cn = chunk_info(d, sc.chunk);
         issue_state<MODE>(pa, stslot(stl), sc.tile * kNP, cn.srow0, cn.ncol, gtid);
         stl = (stl == 2) ? 0 : stl + 1;
-        cursor_next(sc, d, slt);
+        cursor_next_t<ILV>(sc, d, slt);
       } else {
         cp_async_commit();
       }
@@ -828,7 +875,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
         }
       }
       w_arrive(it);  // w(i), fac(i) ready for P3(i)
-      cursor_next(p2c, d, slt);
+      cursor_next_t<ILV>(p2c, d, slt);
     }
   }
 }
@@ -843,14 +890,19 @@ cudaError_t launch_pass_ctf(const PassArgs& a, cudaStream_t st, int pt) {
   const dim3 grid(std::min(a.d.NCH * (a.d.sl1 - a.d.sl0), a.d.ncta));
   const size_t smem = dev::smem_layout(a.d, a.d.nbuf).total;
   void (*kern)(PassArgs, CUtensorMap) = nullptr;
+  // The interleaved instantiation for the A/B passes of large images (Dims::ilv).
+  constexpr bool kIlvOk = CTF == kMaxCT && (MODE == kModeA || MODE == kModeB);
+  const bool ilv = kIlvOk && a.d.ilv != 0;
   if constexpr (MODE == kModeInit || MODE == kModeB) {
     kern = k_pass<MODE, 1, RTW, XT, CTF>;
+    if constexpr (kIlvOk)
+      if (ilv) kern = k_pass<MODE, 1, RTW, XT, CTF, true>;
   } else {
     switch (pt) {
 #define EDAA_PT_CASE(P)                                                                         \
   case P:                                                                                       \
     if constexpr ((PTS == kPtAll || (PTS == kPtLo) == (P <= 5)) && (CTF == kMaxCT || P <= 8)) \
-      kern = k_pass<MODE, P, RTW, XT, CTF>;                                                    \
+      kern = ilv ? k_pass<MODE, P, RTW, XT, CTF, kIlvOk> : k_pass<MODE, P, RTW, XT, CTF>;         \
     break;
       EDAA_PT_CASE(2) EDAA_PT_CASE(3) EDAA_PT_CASE(4) EDAA_PT_CASE(5)
       EDAA_PT_CASE(6) EDAA_PT_CASE(7) EDAA_PT_CASE(8) EDAA_PT_CASE(10) EDAA_PT_CASE(12) EDAA_PT_CASE(16)

@@ -378,7 +378,7 @@ class Device:
         self._check(self.lib.edaa_set_shard_emulation(self.h, int(world)))
 
     def set_pass_order(self, order: int):
-        """Pass work-item order: 0 auto, 1 chunk-major, 2 slice-major (results are
+        """Pass work-item order: 0 auto, 1 chunk-major, 2 slice-major, 3 interleaved (results are
         bitwise identical; include/edaa_b200.h)."""
         self._check(self.lib.edaa_set_pass_order(self.h, int(order)))
 

@@ -427,6 +427,27 @@ def test_pass_item_order_is_bitwise_invisible(runs, p):
         assert all(np.array_equal(a, b) for a, b in zip(u, v))
 
 
+def test_interleaved_item_order_is_bitwise_invisible():
+    """The interleaved A/B pass instantiation (large images: CTA b takes
+    slice-major items b, b+G, …, so the CTAs share X slices in L2) against plain
+    slice-major and chunk-major, on an image with one slice per SM (K = NCH·#SMs)."""
+    x = synth.small_scene(37, 19500, 4, seed=5)
+    cfg = edaa.EnsembleConfig(runs=13, solver=edaa.SolverConfig(endmembers=4, outer_iters=4))
+    seeds, gammas = edaa.ensemble_plan(cfg)
+    d = dev()
+    out = []
+    try:
+        for order in (3, 2, 1):
+            d.set_pass_order(order)
+            out.append(_solve_all(d, x, 4, 4, seeds, gammas))
+    finally:
+        d.set_pass_order(0)
+    for f, t, fit in out[1:]:
+        assert np.array_equal(t, out[0][1]) and fit == out[0][2]
+        for u, v in zip(f, out[0][0]):
+            assert all(np.array_equal(a, b) for a, b in zip(u, v))
+
+
 @pytest.mark.parametrize("first", ["negative", "non-finite"])
 def test_device_validation_reports_the_first_bad_element(first):
     """run_ensemble on an fp32 image validates on the device (edaa_set_image_host_checked)
