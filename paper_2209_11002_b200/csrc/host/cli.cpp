@@ -60,11 +60,10 @@ struct Command {
   std::string name, summary;
   std::vector<Option> options;
 
-  Option& add(std::string opt, std::string help, std::function<void(const std::string&)> assign,
-              bool required = false, std::string shown = {}) {
+  void add(std::string opt, std::string help, std::function<void(const std::string&)> assign,
+           bool required = false, std::string shown = {}) {
     options.push_back(Option{std::move(opt), std::move(help), false, required, std::move(shown),
                              std::move(assign)});
-    return options.back();
   }
   void add_flag(std::string opt, std::string help, bool& target) {
     options.push_back(Option{std::move(opt), std::move(help), true, false, {},
