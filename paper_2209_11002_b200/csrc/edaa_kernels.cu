@@ -179,7 +179,10 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
 // slice partials in kCG contiguous groups added in order (k_combine's order),
 // and forms Z = XAᵀ − Y·AAᵀ.  One launch instead of two, and the rescale
 // factors come from shared memory instead of a global scratch array.
-constexpr int kBR = 8;
+#ifndef EDAA_KBR
+#define EDAA_KBR 8
+#endif
+constexpr int kBR = EDAA_KBR;  // band rows per CTA (a row's slice-sum order does not depend on it)
 
 __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
   griddep_launch_dependents();
@@ -253,18 +256,21 @@ __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
   // kCG·kBR·kQMax = 768 (group, row, column) sums over 256 threads: each thread
   // runs its three with interleaved loads (all of a group's slices in flight).
   {
-    constexpr int kIt = kCG * kBR * kQMax / 256;
+    constexpr int kSums = kCG * kBR * kQMax;
+    constexpr int kIt = (kSums + 255) / 256;
     const double* src[kIt];
     double v[kIt];
     int s0[kIt], len[kIt], xs[kIt], slot[kIt];
     int maxlen = 0;
 #pragma unroll
     for (int q = 0; q < kIt; ++q) {
-      const int e = tid + 256 * q;
+      const int e0 = tid + 256 * q;
+      const bool in = (kSums % 256 == 0) || e0 < kSums;
+      const int e = in ? e0 : 0;
       const int x = e % kQMax, rest = e / kQMax;
       const int rr = rest % kBR, g = rest / kBR;
       s0[q] = (g * S) / kCG;
-      len[q] = (rr < nr) ? ((g + 1) * S) / kCG - s0[q] : 0;
+      len[q] = (in && rr < nr) ? ((g + 1) * S) / kCG - s0[q] : 0;
       src[q] = ca.part_C + static_cast<size_t>(l0 + min(rr, nr - 1)) * d.Qs + col0 + x;
       xs[q] = x;
       slot[q] = (g * kBR + rr) * kQMax + x;
@@ -281,7 +287,8 @@ __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
         }
     }
 #pragma unroll
-    for (int q = 0; q < kIt; ++q) (&red[0][0][0])[slot[q]] = v[q];
+    for (int q = 0; q < kIt; ++q)
+      if ((kSums % 256 == 0) || tid + 256 * q < kSums) (&red[0][0][0])[slot[q]] = v[q];
   }  __syncthreads();
   for (int e = tid; e < nr * kQMax; e += blockDim.x) {
     const int x = e % kQMax, rr = e / kQMax;
