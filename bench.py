@@ -8,6 +8,12 @@ p=4, M=50), the config the metric is quoted on; synthetic seeded data of that
 shape (paper_2209_11002_b200/synth.py).
 
     python bench.py [--gpus N --steps K --warmup W] [--config cfg1] [--impl ours|reference]
+    python bench.py --config cfg4 --strong --gpus N   # north_star sweep: 64 runs split over N GPUs
+
+* ``--gpus N`` outside torchrun (no WORLD_SIZE) re-launches this script under
+  ``torch.distributed.run`` with N processes (one per GPU) and fails loudly
+  when fewer than N CUDA devices are visible; ``n_gpus`` is the number of
+  ranks that actually ran.
 
 * ``value``: run-iterations/s with X resident in HBM, device time (CUDA events
   on the solver stream, L2 flushed with a 256 MB write before every timed
@@ -54,6 +60,9 @@ def parse():
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--outer", type=int, default=100, help="T (default: the reference's 100)")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the config's M runs in total, split over the GPUs "
+                         "(the north_star cfg4 sweep); default: M runs per GPU (weak)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pass-order", type=int, default=0,
@@ -62,6 +71,32 @@ def parse():
                     help="re-normalise the cube in fp64 (as l2_normalize does for a real cube, not "
                          "fp32-exact): the fp64-X pass kernels, the `unmix` CLI path; not the headline")
     return ap.parse_args()
+
+
+def launch_ranks(args, argv):
+    """--gpus N > 1 outside torchrun: one process per GPU under torch.distributed.run.
+    Returns the exit code of the launcher (None when no re-launch is needed)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if have < args.gpus:
+            sys.stderr.write("bench.py: --gpus %d needs %d visible CUDA devices, found %d\n"
+                             % (args.gpus, args.gpus, have))
+            return 2
+    cmd = launcher_cmd(args.gpus, argv)
+    return subprocess.call(cmd, env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
+
+
+def launcher_cmd(n, argv):
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+            "--master-addr", "127.0.0.1", "--master-port", str(port),
+            os.path.join(ROOT, "bench.py")] + list(argv)
 
 
 def dist_env():
@@ -178,15 +213,19 @@ def run_reference_arm(args):
         return 0
     spec, x = scene(args.config)
     cores = os.cpu_count() or 1
-    T = 2  # bounded sample per step: M = cores runs × 2 outer iterations
+    # Bounded sample per step: M = cores concurrent runs at T=4 and at T=1; the
+    # difference is 3 steady-state outer iterations per run (the per-run setup —
+    # B⁰, step sizes, trace[0], fit, μ — cancels), as in cpu_baseline.
     for _ in range(args.warmup):
-        cpu_reference_sample(x, spec, T)
+        cpu_reference_sample(x, spec, 1)
     times = []
     kind = None
     for _ in range(args.steps):
-        dt, its, kind, cores = cpu_reference_sample(x, spec, T)
-        times.append(dt)
+        t4, _, kind, cores = cpu_reference_sample(x, spec, 4)
+        t1, _, _, _ = cpu_reference_sample(x, spec, 1)
+        times.append(max(t4 - t1, 1e-9))
     total = sum(times)
+    T = 3
     value = cores * T * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -194,42 +233,76 @@ def run_reference_arm(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(spec, args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": "%s shape, M=%d runs (one per core) x T=%d per step, "
-                                   "run_ensemble with %d workers%s" % (spec.name, cores, T, cores,
-                                                                      sample_note(spec))},
+                         "sample": "%s shape, M=%d runs (one per core) per step, run_ensemble "
+                                   "with %d workers at T=4 minus T=1 (3 steady-state outer "
+                                   "iterations per run)%s" % (spec.name, cores, cores,
+                                                              sample_note(spec))},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(spec, args, runs=None, T=None):
+def workload_config(spec, args, runs=None, T=None, world=1):
+    strong = getattr(args, "strong", False)
+    total = spec.runs if strong else (runs or spec.runs) * world
     return {"workload": "%s: EDAA ensemble L=%d N=%d p=%d M=%d T=%d K1=K2=5 + model selection"
                         % (spec.name, spec.bands, spec.pixels, spec.endmembers,
-                           runs or spec.runs, T or args.outer),
+                           total, T or args.outer),
             "bands": spec.bands, "pixels": spec.pixels, "endmembers": spec.endmembers,
-            "runs_per_gpu": runs or spec.runs, "outer_iters": T or args.outer,
+            "runs_total": total, "runs_per_gpu": (runs or spec.runs) if not strong else
+            "%d split over %d GPU(s)" % (spec.runs, world), "outer_iters": T or args.outer,
             "inner_iters": [5, 5], "l2_flush": "256 MB write before every timed step",
-            "parallelism": "ensemble runs sharded over GPUs (weak scaling)",
+            "parallelism": ("ensemble runs split over GPUs (strong scaling: fixed total)" if strong
+                            else "ensemble runs sharded over GPUs (weak scaling: M per GPU)"),
             "x_storage": "fp64 (cube re-normalised in fp64: not fp32-exact)" if getattr(args, "x64", False)
                          else "fp32 (fp32-exact normalised cube)"}
 
 
 # ----------------------------------------------------------------------------- our arm
+def selection_margins(fits, mus, oks, slack):
+    """How close the selection was: μ gap of the winner to the runner-up candidate
+    and the nearest fit to the 1.05·fit_min cutoff (relative), ensemble.cpp:71-94."""
+    fits, mus, oks = np.asarray(fits), np.asarray(mus), np.asarray(oks, dtype=bool)
+    if not oks.any():
+        return None
+    fmin = fits[oks].min()
+    cut = slack * fmin
+    cand = np.flatnonzero(oks & (fits <= cut))
+    order = cand[np.argsort(mus[cand], kind="stable")]
+    gap = float((mus[order[1]] - mus[order[0]]) / abs(mus[order[0]])) if len(order) > 1 else None
+    near = float(np.min(np.abs(fits[oks] - cut)) / cut)
+    return {"selected": int(order[0]), "candidates": int(len(cand)),
+            "mu_gap_to_runner_up_rel": gap, "nearest_fit_to_cutoff_rel": near}
+
+
 def main():
     args = parse()
+    rc = launch_ranks(args, sys.argv[1:])
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference_arm(args)
     import torch
     from paper_2209_11002_b200 import edaa
     rank, world, local = dist_env()
+    if torch.cuda.device_count() < world or (args.gpus > 1 and world != args.gpus):
+        raise SystemExit("bench.py: %d ranks for --gpus %d with %d visible CUDA devices"
+                         % (world, args.gpus, torch.cuda.device_count()))
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     spec, x = scene(args.config)
-    L, N, p, M, T = spec.bands, spec.pixels, spec.endmembers, spec.runs, args.outer
+    L, N, p, T = spec.bands, spec.pixels, spec.endmembers, args.outer
+    from paper_2209_11002_b200.distributed import shard_bounds
+    if args.strong:   # the config's runs in total, contiguous blocks per rank
+        first, M = shard_bounds(spec.runs, world, rank)
+        M_total = spec.runs
+    else:             # M runs per rank
+        M = spec.runs
+        first, M_total = rank * M, M * world
     dev = edaa.Device.get(local)
     if args.pass_order:
         dev.set_pass_order(args.pass_order)
@@ -241,22 +314,32 @@ def main():
     x_img = x if args.x64 else x_dev  # host fp64 upload keeps X in fp64 on the device
     torch.cuda.synchronize()
     dev.set_image(x_img)
-    cfg = edaa.EnsembleConfig(runs=M * world, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
-    seeds, gammas = edaa.ensemble_plan(cfg, first=rank * M, count=M)
+    cfg = edaa.EnsembleConfig(runs=M_total, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
+    seeds, gammas = edaa.ensemble_plan(cfg, first=first, count=M)
+    if M == 0:
+        raise SystemExit("bench.py: rank %d has no runs (%d runs over %d GPUs)" % (rank, M_total, world))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
-    def gather_select():
+    Mmax = max(shard_bounds(M_total, world, r)[1] for r in range(world))
+
+    def gather_records():
+        """(fits, mus, oks) of all M_total runs in global order (all_gather over ranks)."""
         recs = [dev.record(m) for m in range(M)]
-        fits = torch.tensor([r.fit_l1 for r in recs], dtype=torch.float64, device=x_dev.device)
-        mus = torch.tensor([r.coherence for r in recs], dtype=torch.float64, device=x_dev.device)
-        oks = torch.tensor([float(r.ok) for r in recs], dtype=torch.float64, device=x_dev.device)
+        loc = torch.zeros(3, Mmax, dtype=torch.float64, device=x_dev.device)
+        loc[0, :M] = torch.tensor([r.fit_l1 for r in recs], dtype=torch.float64)
+        loc[1, :M] = torch.tensor([r.coherence for r in recs], dtype=torch.float64)
+        loc[2, :M] = torch.tensor([float(r.ok) for r in recs], dtype=torch.float64)
         if world > 1:
             import torch.distributed as dist
-            allv = [torch.empty(3, M, dtype=torch.float64, device=x_dev.device) for _ in range(world)]
-            dist.all_gather(allv, torch.stack([fits, mus, oks]))
-            cat = torch.cat(allv, dim=1).cpu().numpy()
+            allv = [torch.empty_like(loc) for _ in range(world)]
+            dist.all_gather(allv, loc)
         else:
-            cat = torch.stack([fits, mus, oks]).cpu().numpy()
+            allv = [loc]
+        parts = [allv[r][:, :shard_bounds(M_total, world, r)[1]] for r in range(world)]
+        return torch.cat(parts, dim=1).cpu().numpy()
+
+    def gather_select():
+        cat = gather_records()
         records = [edaa.RunRecord(i, 0, 0.0, cat[0, i], cat[1, i], 0.0, bool(cat[2, i]), "")
                    for i in range(cat.shape[1])]
         return edaa.select_runs(records, cfg.fit_slack).selected
@@ -301,8 +384,10 @@ def main():
         tt = torch.tensor([t_dev], dtype=torch.float64, device=x_dev.device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_dev = float(tt.item())
-    run_iters = M * world * T * args.steps
+    run_iters = M_total * T * args.steps
     value = run_iters / (t_dev * 1e-3)
+    recs_all = gather_records()
+    margins = selection_margins(recs_all[0], recs_all[1], recs_all[2], cfg.fit_slack)
 
     # ---- e2e through the public API (pinned host X; H2D + solve + select + D2H) ----
     e2e = None
@@ -312,7 +397,7 @@ def main():
         import torch.distributed as dist
         from paper_2209_11002_b200 import distributed
         x_pin = torch.from_numpy(x).pin_memory().numpy()
-        ecfg = edaa.EnsembleConfig(runs=M * world, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
+        ecfg = edaa.EnsembleConfig(runs=M_total, solver=edaa.SolverConfig(endmembers=p, outer_iters=T))
         distributed.run_ensemble_sharded(x_pin, ecfg, device=local)  # warm
         dist.barrier()
         t0 = time.perf_counter()
@@ -321,7 +406,7 @@ def main():
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=x_dev.device)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": M * world * T * args.steps / float(dt.item()), "unit": UNIT,
+        e2e = {"value": M_total * T * args.steps / float(dt.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(x.nbytes + 16 * M),
                "d2h_bytes_per_step": int(8 * (2 * p * N + L * p + (T + 1)) + 32 * M)}
         dev.set_image(x_img)
@@ -376,10 +461,10 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": t_dev / args.steps,
-        "higher_is_better": True, "scaling": "weak",
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
         "vs_baseline": (value / PUBLISHED[spec.name]) if spec.name in PUBLISHED and T == 100 else None,
-        "dtype": "f64", "data": "synthetic", "config": workload_config(spec, args),
-        "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e,
+        "dtype": "f64", "data": "synthetic", "config": workload_config(spec, args, runs=M, world=world),
+        "selection": margins, "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

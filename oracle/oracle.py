@@ -181,6 +181,51 @@ class Oracle:
                       C.byref(eb), self._err, 512))
         return ea.value, eb.value
 
+    # -- reference-only primitives (solver.cpp:65-90,166-188,240-259) -------------
+    def _need_ref(self, what):
+        if self.kind != "reference":
+            raise NotImplementedError("%s: exported by the compiled reference only" % what)
+
+    def _xba(self, name, x, b, a, out_shape):
+        self._need_ref(name)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        out = np.zeros(out_shape)
+        f = self._f(name)
+        f.argtypes = [_dp, _sz, _sz, _dp, _sz, _dp, _dp, C.c_char_p, _sz]
+        self._check(f(x, x.shape[0], x.shape[1], b, b.shape[1], a, out, self._err, 512))
+        return out
+
+    def grad_abundances(self, x, b, a):
+        return self._xba("grad_abundances", x, b, a, (b.shape[1], x.shape[1]))
+
+    def grad_contributions(self, x, b, a):
+        return self._xba("grad_contributions", x, b, a, (x.shape[1], b.shape[1]))
+
+    def objective_l2(self, x, b, a):
+        return float(self._xba("objective_l2", x, b, a, (1,))[0])
+
+    def estimate_abundances(self, x, e, iters, eta):
+        self._need_ref("estimate_abundances")
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        e = np.ascontiguousarray(e, dtype=np.float64)
+        out = np.zeros((e.shape[1], x.shape[1]))
+        f = self._f("estimate_abundances")
+        f.argtypes = [_dp, _sz, _sz, _dp, _sz, _sz, C.c_double, _dp, C.c_char_p, _sz]
+        self._check(f(x, x.shape[0], x.shape[1], e, e.shape[1], int(iters), float(eta), out,
+                      self._err, 512))
+        return out
+
+    def check_iterate(self, m, outer, which):
+        """None if the matrix passes check_iterate, else the reference's message."""
+        self._need_ref("check_iterate")
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        f = self._f("check_iterate")
+        f.argtypes = [_dp, _sz, _sz, _sz, C.c_char_p, C.c_char_p, _sz]
+        rc = f(m, m.shape[0], m.shape[1], int(outer), which.encode(), self._err, 512)
+        return None if rc == 0 else self._err.value.decode("utf-8")
+
     def fit_l1(self, x, e, a):
         x = np.ascontiguousarray(x, dtype=np.float64)
         e = np.ascontiguousarray(e, dtype=np.float64)

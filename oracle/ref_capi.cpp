@@ -26,6 +26,13 @@
 #include "archetype/prng.hpp"
 #include "archetype/solver.hpp"
 
+// solver.cpp is compiled as part of THIS translation unit (included in place
+// from /root/reference by the Makefile's -DREF_SOLVER_CPP, never copied), so
+// the veneer can also reach its anonymous-namespace helpers — check_iterate
+// (solver.cpp:65-90), the per-iterate simplex check that the drop-in's device
+// checks must reproduce message for message.
+#include REF_SOLVER_CPP
+
 namespace ar = archetype;  // renamed to archetype_ref by the Makefile
 
 namespace {
@@ -286,6 +293,82 @@ int oref_sample_gamma(uint64_t seed, const double* set, size_t n_set, size_t dra
     ar::Prng rng(seed);
     const std::vector<double> s(set, set + n_set);
     for (size_t i = 0; i < draws; ++i) out[i] = ar::sample_gamma(rng, s);
+    return 0;
+  } catch (const std::exception& ex) {
+    put_err(ex, err, errlen);
+    return 1;
+  }
+}
+
+// grad_abundances / grad_contributions / objective_l2 (solver.cpp:166-188):
+// b N×p, a p×N; ga p×N, gb N×p.
+int oref_grad_abundances(const double* x, size_t l, size_t n, const double* b, size_t p,
+                         const double* a, double* g, char* err, size_t errlen) {
+  try {
+    ar::ContributionMatrix bm{ar::Matrix(n, p)};
+    std::copy(b, b + n * p, bm.data.values().begin());
+    ar::AbundanceMatrix am{ar::Matrix(p, n)};
+    std::copy(a, a + p * n, am.data.values().begin());
+    copy_out(ar::grad_abundances(make_image(x, l, n), bm, am), g);
+    return 0;
+  } catch (const std::exception& ex) {
+    put_err(ex, err, errlen);
+    return 1;
+  }
+}
+
+int oref_grad_contributions(const double* x, size_t l, size_t n, const double* b, size_t p,
+                            const double* a, double* g, char* err, size_t errlen) {
+  try {
+    ar::ContributionMatrix bm{ar::Matrix(n, p)};
+    std::copy(b, b + n * p, bm.data.values().begin());
+    ar::AbundanceMatrix am{ar::Matrix(p, n)};
+    std::copy(a, a + p * n, am.data.values().begin());
+    copy_out(ar::grad_contributions(make_image(x, l, n), bm, am), g);
+    return 0;
+  } catch (const std::exception& ex) {
+    put_err(ex, err, errlen);
+    return 1;
+  }
+}
+
+int oref_objective_l2(const double* x, size_t l, size_t n, const double* b, size_t p,
+                      const double* a, double* out, char* err, size_t errlen) {
+  try {
+    ar::ContributionMatrix bm{ar::Matrix(n, p)};
+    std::copy(b, b + n * p, bm.data.values().begin());
+    ar::AbundanceMatrix am{ar::Matrix(p, n)};
+    std::copy(a, a + p * n, am.data.values().begin());
+    *out = ar::objective_l2(make_image(x, l, n), bm, am);
+    return 0;
+  } catch (const std::exception& ex) {
+    put_err(ex, err, errlen);
+    return 1;
+  }
+}
+
+// estimate_abundances (solver.cpp:240-259): e L×p → a p×N.
+int oref_estimate_abundances(const double* x, size_t l, size_t n, const double* e, size_t p,
+                             size_t iters, double eta, double* a, char* err, size_t errlen) {
+  try {
+    ar::EndmemberMatrix em{ar::Matrix(l, p)};
+    std::copy(e, e + l * p, em.data.values().begin());
+    copy_out(ar::estimate_abundances(make_image(x, l, n), em, iters, eta).data, a);
+    return 0;
+  } catch (const std::exception& ex) {
+    put_err(ex, err, errlen);
+    return 1;
+  }
+}
+
+// check_iterate (solver.cpp:65-90) on a rows×cols matrix: 0 if it passes, 1 with
+// the reference's message otherwise. which: "abundance" or "contribution".
+int oref_check_iterate(const double* m, size_t rows, size_t cols, size_t outer, const char* which,
+                       char* err, size_t errlen) {
+  try {
+    ar::Matrix mm(rows, cols);
+    std::copy(m, m + rows * cols, mm.values().begin());
+    ar::check_iterate(mm, outer, which);
     return 0;
   } catch (const std::exception& ex) {
     put_err(ex, err, errlen);

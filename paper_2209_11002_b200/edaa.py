@@ -440,6 +440,47 @@ class Device:
                                          A.ctypes.data_as(C.c_void_p), E.shape[1], C.byref(out)))
         return out.value
 
+    def _ba(self, B, A):
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        if B.shape != (self.N, A.shape[0]) or A.shape[1] != self.N:
+            raise EdaaError("shape mismatch (B %s, A %s, N %d)" % (B.shape, A.shape, self.N))
+        return B, A
+
+    def xb(self, B) -> np.ndarray:
+        """X·B (L×p): matmul(x, b), solver.cpp:140."""
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        y = np.zeros((self.L, B.shape[1]))
+        self._check(self.lib.edaa_xb(self.h, B.ctypes.data_as(C.c_void_p), B.shape[1],
+                                     y.ctypes.data_as(C.c_void_p)))
+        return y
+
+    def objective(self, B, A) -> float:
+        """½‖X − XB·A‖² (objective_l2, solver.cpp:184-188)."""
+        B, A = self._ba(B, A)
+        out = C.c_double()
+        self._check(self.lib.edaa_objective(self.h, B.ctypes.data_as(C.c_void_p),
+                                            A.ctypes.data_as(C.c_void_p), A.shape[0], C.byref(out)))
+        return out.value
+
+    def grad_abundances(self, B, A) -> np.ndarray:
+        """−(XB)ᵀ(X − XBA), p×N (solver.cpp:166-172)."""
+        B, A = self._ba(B, A)
+        g = np.zeros(A.shape)
+        self._check(self.lib.edaa_grad_abundances(self.h, B.ctypes.data_as(C.c_void_p),
+                                                  A.ctypes.data_as(C.c_void_p), A.shape[0],
+                                                  g.ctypes.data_as(C.c_void_p)))
+        return g
+
+    def grad_contributions(self, B, A) -> np.ndarray:
+        """−Xᵀ((X − XBA)Aᵀ), N×p (solver.cpp:174-182)."""
+        B, A = self._ba(B, A)
+        g = np.zeros(B.shape)
+        self._check(self.lib.edaa_grad_contributions(self.h, B.ctypes.data_as(C.c_void_p),
+                                                     A.ctypes.data_as(C.c_void_p), A.shape[0],
+                                                     g.ctypes.data_as(C.c_void_p)))
+        return g
+
     def estimate_abundances(self, E, iters: int, eta: float) -> np.ndarray:
         E = np.ascontiguousarray(E, dtype=np.float64)
         A = np.zeros((E.shape[1], self.N))

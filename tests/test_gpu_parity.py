@@ -250,6 +250,42 @@ def test_python_primitives_match_reference(oracle_kinds):
         edaa.estimate_abundances(x, E, 7, 0.0)
 
 
+@pytest.mark.parametrize("L,N,p", [(24, 700, 4), (33, 1001, 2), (60, 2049, 8), (17, 333, 13)])
+def test_primitives_match_compiled_reference(L, N, p):
+    """objective_l2, grad_abundances, grad_contributions (solver.cpp:166-188),
+    estimate_abundances (solver.cpp:240-259) and fit_l1 (ensemble.cpp:29-39)
+    through the C-ABI against the UNMODIFIED reference (liboracle_ref.so) on the
+    same fp32-exact image.  Summation orders differ, so the bar is 1e-12 of
+    each quantity's natural scale (observed ~1e-15)."""
+    from oracle import Oracle, available_kinds
+    if "reference" not in available_kinds():
+        pytest.skip("compiled reference not built")
+    orc = Oracle("reference")
+    rng = np.random.default_rng(1000 + 7 * p + L)
+    E = rng.random((L, p)) + 0.05
+    A = rng.dirichlet(np.full(p, 0.7), N).T
+    x = (E @ A + 0.02 * rng.random((L, N))).astype(np.float32)
+    X = x.astype(np.float64)
+    B = rng.dirichlet(np.ones(N), p).T            # N×p column-stochastic
+    d = dev()
+    d.set_image(x)
+    obj = orc.objective_l2(X, B, A)
+    assert abs(d.objective(B, A) - obj) <= 1e-12 * obj
+    for name in ("grad_abundances", "grad_contributions"):
+        ref = getattr(orc, name)(X, B, A)
+        got = getattr(d, name)(B, A)
+        assert got.shape == ref.shape
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), name
+    y = d.xb(B)
+    assert np.abs(y - X @ B).max() <= 1e-13 * np.abs(X @ B).max()
+    fit = orc.fit_l1(X, E, A)
+    assert abs(d.fit_l1(E, A) - fit) <= 1e-12 * fit
+    for iters, eta in ((1, 0.5), (7, 0.5), (25, 2.0)):
+        ref = orc.estimate_abundances(X, E, iters, eta)
+        got = d.estimate_abundances(E, iters, eta)
+        assert np.abs(got - ref).max() <= 1e-10, (iters, eta)
+
+
 def _solve_all(d, x, p, T, seeds, gammas):
     d.set_image(x)
     d.solve(p, T, 5, 5, seeds, gammas)

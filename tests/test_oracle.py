@@ -155,7 +155,7 @@ def test_port_bitwise_equals_reference_ensemble():
 
 
 @pytest.mark.skipif("port" not in KINDS, reason="port oracle not built")
-@pytest.mark.parametrize("name", [f for f in golden_files() if not f.startswith("cfg")])
+@pytest.mark.parametrize("name", [f for f in golden_files() if not f.startswith(("cfg", "c4"))])
 def test_port_reproduces_golden(name):
     g = load_golden(name)
     x = golden_scene(g).astype(np.float64)
@@ -201,3 +201,43 @@ def test_l2_normalize_error_messages_follow_scan_order(kind):
         Oracle(kind).l2_normalize(y)
     with pytest.raises(OracleError, match="degenerate input: all pixels are zero"):
         Oracle(kind).l2_normalize(np.zeros((3, 5)))
+
+
+@pytest.mark.skipif("reference" not in KINDS, reason="compiled reference not built")
+def test_reference_check_iterate_messages_and_scan_order():
+    """check_iterate (solver.cpp:65-90), reached through the veneer: per column,
+    rows top to bottom, the first non-finite or negative entry wins, the sum
+    check comes after the column; the first failing column decides."""
+    orc = Oracle("reference")
+    a = np.full((3, 4), 1.0 / 3.0)
+    assert orc.check_iterate(a, 1, "abundance") is None
+    m = a.copy(); m[2, 1] = np.nan
+    assert orc.check_iterate(m, 7, "abundance") == "non-finite abundance iterate at outer iteration 7"
+    m = a.copy(); m[1, 2] = -1e-300
+    assert orc.check_iterate(m, 2, "abundance") == "abundance iterate left the simplex at outer iteration 2"
+    m = a.copy(); m[0, 0] += 2e-9
+    assert orc.check_iterate(m, 3, "contribution") == "contribution column sum drifted from 1 at outer iteration 3"
+    m = a.copy(); m[0, 0] += 1e-10          # within tolerance
+    assert orc.check_iterate(m, 3, "abundance") is None
+    m = a.copy(); m[0, 1] += 2e-9; m[2, 1] = np.inf   # same column: the entry check comes first
+    assert orc.check_iterate(m, 4, "abundance").startswith("non-finite")
+    m = a.copy(); m[0, 1] += 2e-9; m[2, 3] = np.inf   # earlier column's drift wins
+    assert "drifted" in orc.check_iterate(m, 4, "abundance")
+
+
+@pytest.mark.skipif("reference" not in KINDS, reason="compiled reference not built")
+def test_reference_primitives_follow_their_definitions():
+    """The new veneer exports (grad_*, objective_l2, estimate_abundances) against
+    their definitions in numpy (solver.cpp:166-188,240-259)."""
+    orc = Oracle("reference")
+    rng = np.random.default_rng(3)
+    x = rng.random((6, 40)); b = rng.dirichlet(np.ones(40), 3).T; a = rng.dirichlet(np.ones(3), 40).T
+    r = x - x @ b @ a
+    assert abs(orc.objective_l2(x, b, a) - 0.5 * np.sum(r * r)) <= 1e-13
+    assert np.abs(orc.grad_abundances(x, b, a) + (x @ b).T @ r).max() <= 1e-13
+    assert np.abs(orc.grad_contributions(x, b, a) + x.T @ (r @ a.T)).max() <= 1e-13
+    e = rng.random((6, 3))
+    est = orc.estimate_abundances(x, e, 5, 0.5)
+    assert est.shape == (3, 40) and np.allclose(est.sum(axis=0), 1.0)
+    with pytest.raises(OracleError, match="eta must be positive"):
+        orc.estimate_abundances(x, e, 5, 0.0)
