@@ -103,6 +103,10 @@ EDAA_API int edaa_set_image_host_f64(edaa_ctx* ctx, const double* x, size_t band
  * reflectance" / "image: negative reflectance", whichever element comes first
  * in row-major order) when the image is not finite and non-negative. */
 EDAA_API int edaa_set_image_host_checked(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels);
+/* _device: x must be device memory of the context's GPU (else EDAA_ERR_INVALID);
+ * the copy is ordered after all work already enqueued on that device (any
+ * stream) and complete when the call returns, so the caller may free x; the
+ * image is validated like _host_checked. */
 EDAA_API int edaa_set_image_device(edaa_ctx* ctx, const float* x, size_t bands, size_t pixels, size_t ld);
 
 /* Ingest on the device: HsiImage::validate + l2_normalize

@@ -916,9 +916,9 @@ int edaa_set_image_host(edaa_ctx* c, const float* x, size_t bands, size_t pixels
   return upload_host(c, x, bands, pixels, 4);
 }
 
-int edaa_set_image_host_checked(edaa_ctx* c, const float* x, size_t bands, size_t pixels) {
-  int rc = upload_host(c, x, bands, pixels, 4);
-  if (rc) return rc;
+// HsiImage::validate (image.cpp:10-27) on the context's fp32 image: the
+// reference's message for the first offending element in row-major order.
+static int check_image_f32(edaa_ctx* c) {
   cudaStream_t st = c->stream;
   EDAA_CUDA(c, ensure(c->in_bad, 24));
   unsigned long long* bad = P<unsigned long long>(c->in_bad);
@@ -936,15 +936,37 @@ int edaa_set_image_host_checked(edaa_ctx* c, const float* x, size_t bands, size_
   return EDAA_OK;
 }
 
+int edaa_set_image_host_checked(edaa_ctx* c, const float* x, size_t bands, size_t pixels) {
+  int rc = upload_host(c, x, bands, pixels, 4);
+  if (rc) return rc;
+  return check_image_f32(c);
+}
+
 int edaa_set_image_host_f64(edaa_ctx* c, const double* x, size_t bands, size_t pixels) {
   return upload_host(c, x, bands, pixels, 8);
 }
 
+// The caller's buffer may have been produced on any stream of this device and
+// may be freed as soon as the call returns: the copy is ordered after ALL work
+// already enqueued on the device (cudaDeviceSynchronize — the C-ABI carries no
+// stream) and finished before returning; the pointer must be device memory of
+// the context's GPU; the image is then validated like the host paths.
 int edaa_set_image_device(edaa_ctx* c, const float* x, size_t bands, size_t pixels, size_t ld) {
   if (!c || !x) return set_err(c, EDAA_ERR_INVALID, "null argument");
   if (ld < pixels) return set_err(c, EDAA_ERR_INVALID, "row pitch smaller than the pixel count");
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, x) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(c, EDAA_ERR_INVALID, "image pointer is not CUDA memory");
+  }
+  if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged)
+    return set_err(c, EDAA_ERR_INVALID, "image pointer is not device memory");
+  if (attr.device != c->device)
+    return set_err(c, EDAA_ERR_INVALID, "image pointer is on another device than the context");
   int rc = prepare_image(c, bands, pixels, 4);
   if (rc) return rc;
+  EDAA_CUDA(c, cudaDeviceSynchronize());  // the producer's writes (any stream) are complete
   k_pad_copy<<<592, 256, 0, c->stream>>>(x, ld, static_cast<float*>(c->X), c->L, c->N, c->Npad);
   EDAA_LAUNCH(c, cudaGetLastError());
   Dims d{};
@@ -953,7 +975,7 @@ int edaa_set_image_device(edaa_ctx* c, const float* x, size_t bands, size_t pixe
   d.Npad = c->Npad;
   d.xbytes = 4;
   EDAA_LAUNCH(c, edaa::launch_xnorm(c->X, c->xnorm, d, c->stream));
-  return EDAA_OK;
+  return check_image_f32(c);  // synchronises c->stream: the caller may free x on return
 }
 
 // Shared by the fp64 and fp32 ingests: upload the raw image as given, then

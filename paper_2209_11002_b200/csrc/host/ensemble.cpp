@@ -110,8 +110,7 @@ using Uploader = std::function<void(detail::Device&)>;
 void solve_shard(Shard& sh, const Uploader& upload, const EnsembleConfig& cfg,
                  const std::vector<std::uint64_t>& seeds, const std::vector<double>& gammas) {
   try {
-    detail::Device& d = *sh.dev;
-    std::lock_guard<std::mutex> lock(d.mu);
+    detail::Device& d = *sh.dev;  // locked by ensemble_on_devices for the whole call
     upload(d);
     const edaa_solve_params prm{cfg.solver.endmembers, cfg.solver.outer_iters,
                                 cfg.solver.inner_iters_a, cfg.solver.inner_iters_b, sh.count,
@@ -133,8 +132,15 @@ namespace {
 
 // The batched solve behind run_ensemble, for an image the uploader puts on
 // every device (host-normalised X, or the raw cube through the device ingest).
+// The reference's run_ensemble is a reentrant pure function: every device this
+// call uses stays locked from the upload through the solve, the selection and
+// the factor / trace download, so a concurrent run(), primitive or
+// run_ensemble() on another thread cannot swap the image or the results in
+// between.  Locks are taken in ascending ordinal (deadlock-free); `held` is
+// device 0's lock when the caller already holds it (ingest → solve).
 std::pair<RunResult, SelectionReport> ensemble_on_devices(const Uploader& upload, std::size_t l,
-                                                          std::size_t n, const EnsembleConfig& config) {
+                                                          std::size_t n, const EnsembleConfig& config,
+                                                          std::unique_lock<std::mutex>* held = nullptr) {
   const std::size_t M = config.runs;
   std::vector<std::uint64_t> seeds(M);
   std::vector<double> gammas(M);
@@ -144,6 +150,9 @@ std::pair<RunResult, SelectionReport> ensemble_on_devices(const Uploader& upload
     gammas[m] = sample_gamma(rng, config.gamma_set);
   }
   const std::size_t ndev = std::min<std::size_t>(static_cast<std::size_t>(detail::device_count()), M);
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (std::size_t g = 0; g < ndev; ++g)
+    if (!(g == 0 && held != nullptr)) locks.emplace_back(detail::device(static_cast<int>(g)).mu);
   std::vector<Shard> shards(ndev);
   for (std::size_t g = 0; g < ndev; ++g) {
     shards[g].first = g * M / ndev;
@@ -179,7 +188,6 @@ std::pair<RunResult, SelectionReport> ensemble_on_devices(const Uploader& upload
   SelectionReport report;
   if (ndev == 1) {  // Algorithm 2's rule on the device (k_select)
     detail::Device& d = *shards[0].dev;
-    std::lock_guard<std::mutex> lock(d.mu);
     std::vector<std::uint8_t> cand(M);
     std::size_t sel = 0;
     double fmin = 0.0;
@@ -210,7 +218,6 @@ std::pair<RunResult, SelectionReport> ensemble_on_devices(const Uploader& upload
   res.contributions.data = Matrix(n, p);
   {
     detail::Device& d = *owner->dev;
-    std::lock_guard<std::mutex> lock(d.mu);
     std::vector<double> traces(owner->count * (config.solver.outer_iters + 1));
     if (edaa_traces(d.ctx, traces.data()) != EDAA_OK ||
         edaa_factors(d.ctx, s - owner->first, res.abundances.data.values().data(),
@@ -267,14 +274,12 @@ static std::pair<RunResult, SelectionReport> ingest_and_solve(const std::functio
     return nz;
   };
   Device& first = device(0);
-  {
-    std::lock_guard<std::mutex> lock(first.mu);
-    zero_pixels = ingest(first);
-  }
+  std::unique_lock<std::mutex> lock(first.mu);  // held from the ingest through the solve
+  zero_pixels = ingest(first);
   shape_check();
   config.validate();
   // Device 0 already holds the normalised image; further devices ingest their own copy.
-  return ensemble_on_devices([&](Device& d) { if (&d != &first) ingest(d); }, l, n, config);
+  return ensemble_on_devices([&](Device& d) { if (&d != &first) ingest(d); }, l, n, config, &lock);
 }
 
 std::pair<RunResult, SelectionReport> run_ensemble_raw(const HsiImage& raw, const EnsembleConfig& config,

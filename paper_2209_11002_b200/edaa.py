@@ -268,6 +268,12 @@ class Device:
         self._check(fn(self.h, xf.ctypes.data_as(C.c_void_p), xf.shape[0], xf.shape[1]))
         self.L, self.N = xf.shape
 
+    def lib_set_image_device_raw(self, x):
+        """Test hook: hand a HOST array to edaa_set_image_device (must be rejected)."""
+        xf = np.ascontiguousarray(x, dtype=np.float32)
+        self._check(self.lib.edaa_set_image_device(self.h, xf.ctypes.data_as(C.c_void_p),
+                                                   xf.shape[0], xf.shape[1], xf.shape[1]))
+
     def ingest(self, x) -> List[int]:
         """Validate + ℓ2-normalise a RAW L×N image on the device (image.cpp:10-47);
         it becomes this device's image.  Returns the zero pixels (left as they are)."""

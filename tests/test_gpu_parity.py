@@ -498,3 +498,30 @@ def test_device_validation_reports_the_first_bad_element(first):
     with pytest.raises(edaa.EdaaError, match="image: %s reflectance" % first):
         edaa.validate_image(x)  # the host restatement agrees
     edaa.run_ensemble(synth.small_scene(12, 300, 3, seed=4), cfg)  # a clean image still solves
+
+
+def test_device_image_upload_is_ordered_checked_and_equal_to_host_upload():
+    """edaa_set_image_device: a tensor produced on another torch stream is copied
+    only after its producer finished, the result equals the host upload bitwise,
+    host memory is rejected, and HsiImage::validate's messages apply."""
+    import torch
+    x = synth.small_scene(bands=30, pixels=900, endmembers=3, seed=5)
+    d = dev()
+    d.set_image(x)
+    d.solve(3, 5, 5, 5, [1], [2.0])
+    ref = d.traces().copy()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        big = torch.empty((30, 900), dtype=torch.float32, device="cuda")
+        torch.cuda._sleep(50_000_000)      # keep the producer busy
+        big.copy_(torch.from_numpy(x).cuda(non_blocking=False))
+    d.set_image(big)                        # must wait for the side stream's copy
+    del big
+    d.solve(3, 5, 5, 5, [1], [2.0])
+    assert np.array_equal(d.traces(), ref)
+    with pytest.raises(edaa.EdaaError, match="not CUDA memory|not device memory"):
+        d.lib_set_image_device_raw(x)
+    bad = torch.from_numpy(x).cuda()
+    bad[3, 7] = -1.0
+    with pytest.raises(edaa.EdaaError, match="image: negative reflectance"):
+        d.set_image(bad)
