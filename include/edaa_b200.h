@@ -59,7 +59,11 @@ enum {
   EDAA_RUN_NONFINITE_B = 2,    /* solver.cpp:72-75 on the contribution block */
   EDAA_RUN_DEGENERATE = 3,     /* solver.cpp:141 */
   EDAA_RUN_SPECTRAL_BAD = 4,   /* matrix.cpp:151-152 */
-  EDAA_RUN_SPECTRAL_NOCONV = 5 /* matrix.cpp:186-189 */
+  EDAA_RUN_SPECTRAL_NOCONV = 5, /* matrix.cpp:186-189 */
+  EDAA_RUN_SIMPLEX_A = 6,      /* "abundance iterate left the simplex ..."      solver.cpp:77-81 */
+  EDAA_RUN_SIMPLEX_B = 7,      /* "contribution iterate left the simplex ..."   solver.cpp:77-81 */
+  EDAA_RUN_DRIFT_A = 8,        /* "abundance column sum drifted from 1 ..."     solver.cpp:84-88 */
+  EDAA_RUN_DRIFT_B = 9         /* "contribution column sum drifted from 1 ..."  solver.cpp:84-88 */
 };
 
 typedef struct {
@@ -206,6 +210,17 @@ EDAA_API int edaa_grad_contributions(edaa_ctx* ctx, const double* b, const doubl
 EDAA_API int edaa_fit_l1(edaa_ctx* ctx, const double* e, const double* a, size_t p, double* out);
 EDAA_API int edaa_estimate_abundances(edaa_ctx* ctx, const double* e, size_t p, size_t iters,
                                       double eta, double* a);
+
+/* check_iterate (reference solver.cpp:65-90: the simplex / finiteness check the
+ * solver applies after every inner update) on a host row-major rows×cols
+ * matrix whose COLUMNS are the simplex vectors, evaluated on the device by the
+ * per-column check the solve's kernels use.  *code = EDAA_RUN_OK, or the code of
+ * the first failing check in the reference's scan order (column by column; per
+ * entry finite then >= 0; then |Σ − 1| <= 1e-9) for the abundance block
+ * (contribution = 0) or the contribution block (contribution != 0); `message`
+ * receives the reference's text for it with `outer` as the iteration index. */
+EDAA_API int edaa_check_iterate(edaa_ctx* ctx, const double* m, size_t rows, size_t cols, size_t outer,
+                                int contribution, int* code, char* message, size_t message_len);
 
 /* Instrumentation.  With profiling on, every pass launch is bracketed by CUDA
  * events on edaa_stream(); edaa_profile_read returns, per pass kind, the

@@ -77,6 +77,8 @@ SIGNATURES = [
     ("edaa_fit_l1", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     ("edaa_estimate_abundances", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
                                            C.c_double, C.c_void_p]),
+    ("edaa_check_iterate", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
+                                     C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
     ("edaa_profile_enable", C.c_int, [C.c_void_p, C.c_int]),
     ("edaa_profile_read", C.c_int, [C.c_void_p, C.POINTER(ProfileC)]),
     ("edaa_launch_count", C.c_uint64, [C.c_void_p]),

@@ -232,6 +232,18 @@ __global__ void k_dmma_peak(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// check_iterate's failure (solver.cpp:65-90) from a device fail key.
+int fail_key_code(unsigned long long key, size_t* outer) {
+  const unsigned tb = edaa::fail_key_tb(key);
+  *outer = tb >> 1;
+  const bool b = tb & 1u;
+  switch (edaa::fail_key_kind(key)) {
+    case edaa::kFailNonFinite: return b ? EDAA_RUN_NONFINITE_B : EDAA_RUN_NONFINITE_A;
+    case edaa::kFailNegative: return b ? EDAA_RUN_SIMPLEX_B : EDAA_RUN_SIMPLEX_A;
+    default: return b ? EDAA_RUN_DRIFT_B : EDAA_RUN_DRIFT_A;
+  }
+}
+
 std::string run_message(int code, size_t outer, double value) {
   char buf[192];
   switch (code) {
@@ -240,6 +252,18 @@ std::string run_message(int code, size_t outer, double value) {
       return buf;
     case EDAA_RUN_NONFINITE_B:
       std::snprintf(buf, sizeof buf, "non-finite contribution iterate at outer iteration %zu", outer);
+      return buf;
+    case EDAA_RUN_SIMPLEX_A:
+      std::snprintf(buf, sizeof buf, "abundance iterate left the simplex at outer iteration %zu", outer);
+      return buf;
+    case EDAA_RUN_SIMPLEX_B:
+      std::snprintf(buf, sizeof buf, "contribution iterate left the simplex at outer iteration %zu", outer);
+      return buf;
+    case EDAA_RUN_DRIFT_A:
+      std::snprintf(buf, sizeof buf, "abundance column sum drifted from 1 at outer iteration %zu", outer);
+      return buf;
+    case EDAA_RUN_DRIFT_B:
+      std::snprintf(buf, sizeof buf, "contribution column sum drifted from 1 at outer iteration %zu", outer);
       return buf;
     case EDAA_RUN_DEGENERATE:
       return "degenerate initialization: X\xc2\xb7" "B0 is zero";
@@ -479,7 +503,7 @@ edaa::PassArgs pass_args(edaa_ctx* c, int t, const double* W) {
   return a;
 }
 
-edaa::CombineArgs combine_args(edaa_ctx* c, int t, int mode, int trace_index) {
+edaa::CombineArgs combine_args(edaa_ctx* c, int t, int mode, int trace_index, int kin = 0) {
   edaa::CombineArgs a{};
   a.d = c->d;
   a.t = t;
@@ -500,6 +524,7 @@ edaa::CombineArgs combine_args(edaa_ctx* c, int t, int mode, int trace_index) {
   a.trace_stride = static_cast<int>(c->T + 1);
   a.trace_index = trace_index;
   a.fail_key = P<unsigned long long>(c->fail_key);
+  a.kin = kin;
   return a;
 }
 
@@ -762,7 +787,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
       edaa::PassArgs pb = pass_args(c, ti, P<double>(c->Z));
       rc = run_pass(c, edaa::kModeB, pb);
       if (rc) return rc;
-      EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0), st));
+      EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0, static_cast<int>(k)), st));
       if (k == prm->inner_iters_b) EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostG), st));
       if (hook) {
         rc = download_b(c, hook);
@@ -1250,8 +1275,7 @@ int edaa_run_record_get(edaa_ctx* c, size_t run, edaa_run_record* out) {
   int code = c->h_fail_code[run];
   size_t outer = 0;
   if (code == EDAA_RUN_OK && c->h_fail_key[run] != ~0ull) {
-    outer = static_cast<size_t>(c->h_fail_key[run] >> 1);
-    code = (c->h_fail_key[run] & 1ull) ? EDAA_RUN_NONFINITE_B : EDAA_RUN_NONFINITE_A;
+    code = fail_key_code(c->h_fail_key[run], &outer);
   }
   out->fail_code = code;
   out->fail_outer = outer;
@@ -1448,6 +1472,33 @@ int edaa_grad_contributions(edaa_ctx* c, const double* b, const double* a, size_
                                        static_cast<int>(p), c->stream), 2);
   EDAA_CUDA(c, cudaMemcpyAsync(g, c->pr_g.p, p * c->N * 8, cudaMemcpyDeviceToHost, c->stream));
   EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  return EDAA_OK;
+}
+
+int edaa_check_iterate(edaa_ctx* c, const double* m, size_t rows, size_t cols, size_t outer,
+                       int contribution, int* code, char* message, size_t message_len) {
+  if (!c || !m || !code || rows == 0 || cols == 0) return c ? set_err(c, EDAA_ERR_INVALID, "check_iterate: bad argument") : EDAA_ERR_INVALID;
+  if (rows >= (1ull << 34) - 1 || cols >= (1ull << 28))
+    return set_err(c, EDAA_ERR_UNSUPPORTED, "check_iterate: matrix too large");
+  EDAA_CUDA(c, cudaSetDevice(c->device));
+  EDAA_CUDA(c, ensure(c->pr_g, rows * cols * 8 + 8));
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(P<double>(c->pr_g) + rows * cols);
+  EDAA_CUDA(c, cudaMemcpyAsync(c->pr_g.p, m, rows * cols * 8, cudaMemcpyHostToDevice, c->stream));
+  EDAA_CUDA(c, cudaMemsetAsync(key, 0xFF, 8, c->stream));
+  EDAA_LAUNCH(c, edaa::launch_check_iterate(P<double>(c->pr_g), static_cast<int>(rows), static_cast<int>(cols),
+                                            key, c->stream));
+  unsigned long long h = 0;
+  EDAA_CUDA(c, cudaMemcpyAsync(&h, key, 8, cudaMemcpyDeviceToHost, c->stream));
+  EDAA_CUDA(c, cudaStreamSynchronize(c->stream));
+  *code = EDAA_RUN_OK;
+  if (h != ~0ull) {
+    switch (static_cast<unsigned>(h & 3ull)) {
+      case edaa::kFailNonFinite: *code = contribution ? EDAA_RUN_NONFINITE_B : EDAA_RUN_NONFINITE_A; break;
+      case edaa::kFailNegative: *code = contribution ? EDAA_RUN_SIMPLEX_B : EDAA_RUN_SIMPLEX_A; break;
+      default: *code = contribution ? EDAA_RUN_DRIFT_B : EDAA_RUN_DRIFT_A; break;
+    }
+  }
+  if (message && message_len) std::snprintf(message, message_len, "%s", run_message(*code, outer, 0.0).c_str());
   return EDAA_OK;
 }
 

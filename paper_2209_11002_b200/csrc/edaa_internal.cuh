@@ -49,7 +49,28 @@ enum FailCode : int {
   kDegenerateInit = 3,   // "degenerate initialization: X·B0 is zero"  solver.cpp:141
   kSpectralBad = 4,      // "spectral_norm: matrix must be finite and nonzero"  matrix.cpp:151
   kSpectralNoConv = 5,   // "spectral_norm: no convergence after ..."  matrix.cpp:186-189
+  kSimplexA = 6,         // "abundance iterate left the simplex at outer iteration t"  solver.cpp:77-81
+  kSimplexB = 7,         // "contribution iterate left the simplex ..."
+  kDriftA = 8,           // "abundance column sum drifted from 1 at outer iteration t"  solver.cpp:84-88
+  kDriftB = 9,           // "contribution column sum drifted from 1 ..."
 };
+
+// Per-run failure key of check_iterate (solver.cpp:65-90): the reference stops
+// at the FIRST failing check of its scan (outer t, block A then B, inner step k,
+// column, then per entry: finite, >= 0; then the column sum).  Every device
+// check posts its position with atomicMin, so the surviving key is that first
+// failure:  [t<<1|block : 23][k : 6][position : 33][kind : 2].
+// Position: A block = pixel·32 + entry (31 = the column-sum check);
+//           B block = endmember·2^28 + pixel (2^28−1 = the column-sum check).
+enum FailKind : unsigned { kFailNonFinite = 0, kFailNegative = 1, kFailDrift = 2 };
+constexpr double kSimplexTol = 1e-9;  // solver.cpp:84
+__host__ __device__ inline unsigned long long fail_key_make(unsigned tb, unsigned k, unsigned long long pos,
+                                                            unsigned kind) {
+  return (static_cast<unsigned long long>(tb) << 41) | (static_cast<unsigned long long>(k < 63u ? k : 63u) << 35) |
+         ((pos & ((1ull << 33) - 1)) << 2) | kind;
+}
+inline unsigned fail_key_tb(unsigned long long key) { return static_cast<unsigned>(key >> 41); }
+inline unsigned fail_key_kind(unsigned long long key) { return static_cast<unsigned>(key & 3ull); }
 
 struct Dims {
   int L, Lpad, N, Npad;
@@ -85,7 +106,7 @@ struct PassArgs {
   double* part_m;         // [nslices][Qs]
   double* part_S;         // [nslices][Qs]
   double* part_obj;       // [nslices][M]
-  unsigned long long* fail_key;  // [M]  min over (t<<1 | block)
+  unsigned long long* fail_key;  // [M]  min over fail_key_make(...)
   double* observe_A;      // optional [K1][p][Npad] inner iterates (M == 1 observed mode)
   unsigned long long* kprof;  // optional cycle accounting (development)
   int dbg;                    // development switches (EDAA_DBG): 1 no DMMA, 2 no B update
@@ -95,6 +116,7 @@ struct PassArgs {
 struct CombineArgs {
   Dims d;
   int t;
+  int kin;   // inner B step (orders failures of one outer iteration; 0 otherwise)
   int mode;  // kModeA: plain sums (XAt, AAt, objective); kModeB/kModeInit: LSE combine into Y
   const double* part_C;
   const double* part_m;
@@ -184,6 +206,8 @@ cudaError_t launch_grad_a(const double* Y, const double* R, double* G, int L, in
                           cudaStream_t st);
 cudaError_t launch_grad_b(const void* X, int xbytes, const double* R, const double* A, double* rat,
                           double* G, int L, int N, int Npad, int p, cudaStream_t st);
+cudaError_t launch_check_iterate(const double* m, int rows, int cols, unsigned long long* key,
+                                 cudaStream_t st);
 cudaError_t launch_estimate(const void* X, int xbytes, const double* E, double* A, int L, int N,
                             int Npad, int p, int iters, double eta, cudaStream_t st);
 constexpr int kMaxSmem = 232448;  // sm_100 opt-in dynamic shared memory per block

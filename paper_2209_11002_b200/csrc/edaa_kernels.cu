@@ -34,6 +34,21 @@ namespace {
 
 using namespace dev;
 
+// check_iterate on a contribution column held as logits + normaliser
+// (solver.cpp:65-90): b_j = e^{ℓ_j − m}/S.  Non-finite: the column max or sum
+// is not finite (a NaN/Inf logit poisons both).  Negative entries cannot occur
+// (an exponential over a positive sum).  Drift: the mass of the normalised
+// column, accumulated slice by slice, is further than 1e-9 from 1.
+__device__ __forceinline__ void post_column_check(const CombineArgs& ca, int r, int i, double m, double Ssum,
+                                                  double nsum) {
+  const unsigned tb = (static_cast<unsigned>(ca.t) << 1) | 1u;
+  const unsigned long long col = static_cast<unsigned long long>(i) << 28;
+  if (!(isfinite(m) && isfinite(Ssum) && Ssum > 0.0))
+    atomicMin(ca.fail_key + r, fail_key_make(tb, ca.kin, col, kFailNonFinite));
+  else if (!(fabs(nsum - 1.0) <= kSimplexTol))
+    atomicMin(ca.fail_key + r, fail_key_make(tb, ca.kin, col | ((1ull << 28) - 1), kFailDrift));
+}
+
 // the slices, fixed xor-tree merge (deterministic).
 __global__ void k_colnorm(CombineArgs ca) {
   griddep_launch_dependents();
@@ -54,15 +69,19 @@ __global__ void k_colnorm(CombineArgs ca) {
     Ssum += ca.part_S[static_cast<size_t>(sl) * d.Qs + col] * f;
   }
   Ssum = warp_sum(Ssum);
+  // Mass of the normalised column b = e^{ℓ−m}/S, slice by slice (the drift check).
+  const double inv = 1.0 / Ssum;
+  double nsum = 0.0;
+  for (int sl = lane; sl < S; sl += 32)
+    nsum += ca.part_S[static_cast<size_t>(sl) * d.Qs + col] * ca.fac[static_cast<size_t>(sl) * d.Qs + col] * inv;
+  nsum = warp_sum(nsum);
   if (lane != 0) return;
   ca.colm[col] = m;
   ca.colS[col] = Ssum;
   ca.collogS[col] = log(Ssum);
-  // A column of a real run must have a finite max and a finite positive sum.
   const int chunk = col / d.QCpad, c = col % d.QCpad;
   const int r = chunk * d.RC + c / d.p;
-  if (c < d.RC * d.p && r < d.M && !(isfinite(m) && isfinite(Ssum) && Ssum > 0.0))
-    atomicMin(ca.fail_key + r, (static_cast<unsigned long long>(ca.t) << 1) | 1ull);
+  if (c < d.RC * d.p && r < d.M) post_column_check(ca, r, c % d.p, m, Ssum, nsum);
 }
 
 // Row sums over slices (fixed order): A mode → XAt / AAt; B/init → Y = Σ C_s·fac_s / S.
@@ -237,15 +256,25 @@ __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
     }
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) Ssum += __shfl_xor_sync(0xffffffffu, Ssum, o);
+    if (blockIdx.y == 0) {  // one CTA per chunk runs check_iterate on the chunk's columns
+      const double inv = 1.0 / Ssum;
+      double nsum = 0.0;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int sl = t8 + 8 * k;
+        if (sl < S) nsum += sv[k] * facs[sl * kQMax + cc] * inv;
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      const int r = chunk * d.RC + cc / d.p;
+      if (t8 == 0 && cc < d.RC * d.p && r < d.M) post_column_check(ca, r, cc % d.p, m, Ssum, nsum);
+    }
     if (t8 == 0) {
       cS[cc] = Ssum;
       if (blockIdx.y == 0) {
         ca.colm[col] = m;
         ca.colS[col] = Ssum;
         ca.collogS[col] = log(Ssum);
-        const int r = chunk * d.RC + cc / d.p;
-        if (cc < d.RC * d.p && r < d.M && !(isfinite(m) && isfinite(Ssum) && Ssum > 0.0))
-          atomicMin(ca.fail_key + r, (static_cast<unsigned long long>(ca.t) << 1) | 1ull);
       }
     }
   }

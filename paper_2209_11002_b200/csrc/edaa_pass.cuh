@@ -155,12 +155,37 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     for (int o = 1; o < TPP; o <<= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
     // total ∈ [1e-30, p] (every factor ≤ 1, the largest ≥ 1e-30): a normal number.
     const double inv = __drcp_rn(total);  // IEEE 1/total (= the division's value)
+    // check_iterate (solver.cpp:65-90) on this pixel's column: every entry
+    // finite and >= 0, |Σ − 1| <= 1e-9.  A NaN/Inf entry makes the sum
+    // NaN/Inf, so the fast path is one sum, one sign test and one compare;
+    // the first failing check in the reference's scan order is resolved only
+    // when something failed (post_simplex_failure).
+    double csum = 0.0;
+    bool neg = false;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       if (own[e]) {
         a[e] *= inv;
-        bad |= !isfinite(a[e]);
+        csum += a[e];
+        neg |= a[e] < 0.0;
       }
+    }
+#pragma unroll
+    for (int o = 1; o < TPP; o <<= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    if ((neg || !(fabs(csum - 1.0) <= kSimplexTol)) && valid && !bad) {
+      bad = true;  // later inner steps of this pixel can only fail later in the scan order
+      unsigned long long key = ~0ull;
+#pragma unroll
+      for (int e = EPT - 1; e >= 0; --e) {
+        if (own[e] && !(isfinite(a[e]) && a[e] >= 0.0))
+          key = fail_key_make((static_cast<unsigned>(pa.t) << 1), k,
+                              (static_cast<unsigned long long>(pix) << 5) | static_cast<unsigned>(sub * EPT + e),
+                              isfinite(a[e]) ? kFailNegative : kFailNonFinite);
+      }
+      if (key == ~0ull)  // entries fine on this lane: the column-sum check comes after all of them
+        key = fail_key_make((static_cast<unsigned>(pa.t) << 1), k,
+                            (static_cast<unsigned long long>(pix) << 5) | 31u, kFailDrift);
+      atomicMin(pa.fail_key + r, key);
     }
     if (pa.observe_A != nullptr && valid) {
 #pragma unroll
@@ -174,7 +199,6 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     aGa += __shfl_xor_sync(0xffffffffu, aGa, o);
   }
   if (UPDATE) {
-    if (bad && valid) atomicMin(pa.fail_key + r, static_cast<unsigned long long>(pa.t) << 1);
     const size_t base = static_cast<size_t>(r) * p * d.Npad + pix;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {

@@ -125,6 +125,27 @@ __global__ void k_estimate(const XT* X, const double* E, double* A, int L, int N
   for (int i = 0; i < p; ++i) A[static_cast<size_t>(i) * N + j] = a[i];
 }
 
+// check_iterate (solver.cpp:65-90) on a row-major d×n matrix, one column per
+// thread, entries and the column sum in the reference's order.  The first
+// failing check of the reference's column-by-column scan survives the
+// atomicMin: key = column·2^36 + entry·4 + kind (entry = 2^34−1 for the sum).
+__global__ void k_check_iterate(const double* m, int d, int n, unsigned long long* key) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double sum = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const double v = m[static_cast<size_t>(i) * n + j];
+    if (!(isfinite(v) && v >= 0.0)) {
+      atomicMin(key, (static_cast<unsigned long long>(j) << 36) | (static_cast<unsigned long long>(i) << 2) |
+                         (isfinite(v) ? kFailNegative : kFailNonFinite));
+      return;
+    }
+    sum = __dadd_rn(sum, v);
+  }
+  if (!(fabs(sum - 1.0) <= kSimplexTol))
+    atomicMin(key, (static_cast<unsigned long long>(j) << 36) | (((1ull << 34) - 1) << 2) | kFailDrift);
+}
+
 inline int blocks_for(size_t n, int threads) {
   return static_cast<int>(std::min<size_t>((n + threads - 1) / threads, 4096));
 }
@@ -161,6 +182,12 @@ cudaError_t launch_grad_b(const void* X, int xbytes, const double* R, const doub
     k_grad_b<<<(N + 127) / 128, 128, 0, st>>>(static_cast<const double*>(X), rat, G, L, N, Npad, p);
   else
     k_grad_b<<<(N + 127) / 128, 128, 0, st>>>(static_cast<const float*>(X), rat, G, L, N, Npad, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_iterate(const double* m, int rows, int cols, unsigned long long* key,
+                                 cudaStream_t st) {
+  k_check_iterate<<<(cols + 127) / 128, 128, 0, st>>>(m, rows, cols, key);
   return cudaGetLastError();
 }
 

@@ -495,6 +495,19 @@ class Device:
                                                       A.ctypes.data_as(C.c_void_p)))
         return A
 
+    def check_iterate(self, m, outer: int, which: str) -> str:
+        """check_iterate (solver.cpp:65-90) on the columns of `m`, on the device: '' if the
+        iterate is fine, else the reference's message for the first failing check."""
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        if which not in ("abundance", "contribution"):
+            raise ValueError("which must be 'abundance' or 'contribution'")
+        code = C.c_int(0)
+        buf = C.create_string_buffer(192)
+        self._check(self.lib.edaa_check_iterate(self.h, m.ctypes.data_as(C.c_void_p), m.shape[0], m.shape[1],
+                                                int(outer), int(which == "contribution"), C.byref(code),
+                                                buf, 192))
+        return buf.value.decode() if code.value else ""
+
 
 def _result(dev: Device, run_idx: int, seed: int, gamma: float, traces) -> RunResult:
     A, B, E = dev.factors(run_idx)
