@@ -156,24 +156,26 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     // total ∈ [1e-30, p] (every factor ≤ 1, the largest ≥ 1e-30): a normal number.
     const double inv = __drcp_rn(total);  // IEEE 1/total (= the division's value)
     // check_iterate (solver.cpp:65-90) on this pixel's column: every entry
-    // finite and >= 0, |Σ − 1| <= 1e-9.  A NaN/Inf entry makes the sum
-    // NaN/Inf, so the fast path is one sum, one sign test and one compare;
-    // the first failing check in the reference's scan order is resolved only
-    // when something failed (post_simplex_failure).
+    // finite and >= 0, |Σ − 1| <= 1e-9.  The fast path only TRIGGERS the exact
+    // checks, and does so on the integer pipe (the fp64 pipe is the A pass's
+    // bottleneck): the OR of the entries' sign bits, and the high word of
+    // |Σ − 1| against that of 1e-9 (NaN/Inf entries make Σ NaN/Inf, whose high
+    // word is above every finite one).  post_simplex_failure then re-evaluates the
+    // reference's conditions exactly and resolves its scan order.
     double csum = 0.0;
-    bool neg = false;
+    int signs = 0;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       if (own[e]) {
         a[e] *= inv;
         csum += a[e];
-        neg |= a[e] < 0.0;
+        signs |= __double2hiint(a[e]);
       }
     }
 #pragma unroll
     for (int o = 1; o < TPP; o <<= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
-    if ((neg || !(fabs(csum - 1.0) <= kSimplexTol)) && valid && !bad) {
-      bad = true;  // later inner steps of this pixel can only fail later in the scan order
+    constexpr int kTolHi = 0x3E112E0B;  // high word of 1e-9 (0x3E112E0BE826D695)
+    if (((signs < 0) | ((__double2hiint(csum - 1.0) & 0x7fffffff) >= kTolHi)) && valid && !bad) {
       unsigned long long key = ~0ull;
 #pragma unroll
       for (int e = EPT - 1; e >= 0; --e) {
@@ -182,10 +184,14 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
                               (static_cast<unsigned long long>(pix) << 5) | static_cast<unsigned>(sub * EPT + e),
                               isfinite(a[e]) ? kFailNegative : kFailNonFinite);
       }
-      if (key == ~0ull)  // entries fine on this lane: the column-sum check comes after all of them
+      // entries fine on this lane: the column-sum check comes after all of them
+      if (key == ~0ull && !(fabs(csum - 1.0) <= kSimplexTol))
         key = fail_key_make((static_cast<unsigned>(pa.t) << 1), k,
                             (static_cast<unsigned long long>(pix) << 5) | 31u, kFailDrift);
-      atomicMin(pa.fail_key + r, key);
+      if (key != ~0ull) {
+        bad = true;  // later inner steps of this pixel can only fail later in the scan order
+        atomicMin(pa.fail_key + r, key);
+      }
     }
     if (pa.observe_A != nullptr && valid) {
 #pragma unroll

@@ -219,6 +219,18 @@ int unmix(const UnmixArgs& args, std::ostream& out) {
     report.pixels = cube.pixels();
     report.spatial = cube.spatial;
   }
+  // This build's device kernels are compiled for p <= edaa_max_endmembers() and
+  // L <= edaa_max_bands() (README "Limits"); there is no CPU fallback, so a
+  // shape outside them is refused here, before any device work, naming the limit.
+  if (args.endmembers > edaa_max_endmembers()) {
+    throw Error("unmix: --endmembers " + std::to_string(args.endmembers) + " is above this build's limit of " +
+                std::to_string(edaa_max_endmembers()) + " endmembers (the B200 pass kernels are compiled for p <= " +
+                std::to_string(edaa_max_endmembers()) + ")");
+  }
+  if (report.bands > edaa_max_bands()) {
+    throw Error("unmix: the cube has " + std::to_string(report.bands) + " bands, above this build's limit of " +
+                std::to_string(edaa_max_bands()) + " (the B200 pass kernels keep one band column tile in shared memory)");
+  }
   EnsembleConfig& cfg = report.config;
   cfg.runs = args.runs;
   cfg.base_seed = args.seed;

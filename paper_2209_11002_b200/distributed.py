@@ -94,28 +94,31 @@ def run_ensemble_sharded(x, config: edaa.EnsembleConfig, group=None,
     width = -(-config.runs // world)
     backend = dist.get_backend(group)
     tdev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    mine = torch.full((4, width), float("nan"), dtype=torch.float64, device=tdev)
+    mine_h = np.full((5, width), np.nan)
     for k, rec in enumerate(batch.records):
-        mine[0, k] = rec.fit_l1
-        mine[1, k] = rec.coherence
-        mine[2, k] = 1.0 if rec.ok else 0.0
-        mine[3, k] = rec.gamma
+        mine_h[:, k] = (rec.fit_l1, rec.coherence, 1.0 if rec.ok else 0.0, rec.gamma, rec.wall_ms)
+    mine = torch.from_numpy(mine_h).to(tdev)
     gathered = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(gathered, mine, group=group)
     table = [g.cpu().numpy() for g in gathered]
     seeds, gammas = edaa.ensemble_plan(config)
+    # Failed runs carry the reference's error text (ensemble.cpp:150-155 →
+    # report.json "error"): gathered as objects only when some run failed, so the
+    # healthy path stays one tensor all-gather and every rank builds the SAME report.
+    errors = [{} for _ in range(world)]
+    if any(not bool(np.all(t[2, :shard_bounds(config.runs, world, r)[1]] == 1.0)) for r, t in enumerate(table)):
+        dist.all_gather_object(errors, {rec.index: rec.error for rec in batch.records if not rec.ok},
+                               group=group)
     records = []
     for r in range(world):
         f, c = shard_bounds(config.runs, world, r)
         for k in range(c):
             m = f + k
             ok = bool(table[r][2, k] == 1.0)
-            err = ""
-            if r == rank:
-                err = batch.records[k].error
             records.append(edaa.RunRecord(m, seeds[m], float(table[r][3, k]),
                                           float(table[r][0, k]) if ok else 0.0,
-                                          float(table[r][1, k]) if ok else 0.0, 0.0, ok, err))
+                                          float(table[r][1, k]) if ok else 0.0,
+                                          float(table[r][4, k]), ok, errors[r].get(m, "")))
     report = edaa.select_runs(records, config.fit_slack)
 
     # ---- the selected run's factors from its owner ----

@@ -76,6 +76,48 @@ def test_sharded_selection_matches_single_process(tmp_path, runs):
         assert np.array_equal(r["trace"], ref.trace)
 
 
+def failing_local_solver(x, config, first, count):
+    """The oracle solver, with ensemble member 5 reported as failed (its owner
+    is rank 1 at world 2) and a distinct wall time per run."""
+    batch = oracle_local_solver(x, config, first, count)
+    for rec in batch.records:
+        rec.wall_ms = 10.0 + rec.index
+        if rec.index == 5:
+            rec.ok, rec.fit_l1, rec.coherence = False, 0.0, 0.0
+            rec.error = "non-finite abundance iterate at outer iteration 3"
+    return batch
+
+
+def _report_worker(rank, world, port, out):
+    import json
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x = synth.small_scene(16, 200, 3, seed=4)
+    cfg = edaa.EnsembleConfig(runs=7, solver=edaa.SolverConfig(endmembers=3, outer_iters=4))
+    _, rep = distributed.run_ensemble_sharded(x, cfg, local_solver=failing_local_solver)
+    with open(out % rank, "w") as f:
+        json.dump([[r.index, r.seed, r.gamma, r.fit_l1, r.coherence, r.wall_ms, r.ok, r.error]
+                   for r in rep.per_run] + [rep.selected, rep.candidate_set], f)
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not __import__("oracle").available_kinds(), reason="oracle not built")
+def test_every_rank_builds_the_same_report_including_failed_runs(tmp_path):
+    """A failed run's error text (report.json "error", outputs.cpp:33-35) and the
+    wall times reach every rank: the SelectionReport is identical on all of them."""
+    import json
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "rep%d.json")
+    mp.spawn(_report_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    r0, r1 = json.load(open(out % 0)), json.load(open(out % 1))
+    assert r0 == r1
+    assert r0[5][6] is False and r0[5][7] == "non-finite abundance iterate at outer iteration 3"
+    assert [rec[5] for rec in r0[:7]] == [10.0 + i for i in range(7)]
+    assert 5 not in r0[-1]
+
+
 # ---- pixel sharding of one solve (distributed.run_pixel_sharded) -----------------
 
 @pytest.mark.parametrize("pixels", [1, 31, 500, 4000, 10000, 94249, 1048576])
