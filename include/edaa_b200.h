@@ -180,6 +180,18 @@ EDAA_API int edaa_nccl_unique_id(void* out, size_t bytes /* >= 128 */);
 EDAA_API int edaa_set_pixel_shard(edaa_ctx* ctx, const void* id, size_t bytes, int rank, int world);
 EDAA_API int edaa_shard_pixels(edaa_ctx* ctx, size_t* first, size_t* end);
 EDAA_API int edaa_set_shard_emulation(edaa_ctx* ctx, int world);
+/* What the ranks exchange after every pass.
+ *   0 (default): ALLREDUCE — BASELINE north_star's shape.  Every rank reduces
+ *     the partial sums of its own pixel slices to one block (Y or XAᵀ: L×Q;
+ *     AAᵀ: Q×Q on the run diagonal; the 2·Q softmax normaliser terms (m, S);
+ *     the M objective terms), the column maxima are max-allreduced, the blocks
+ *     rescaled to them and sum-allreduced: ~(L+24)·Q·8 bytes per pass and rank
+ *     (cfg4 single run: 47.6 KB).  Equal to the single-device solve to
+ *     rounding (the cross-rank sum order is NCCL's).
+ *   1: BROADCAST of every slice partial (nslices·(L+24)·Q·8 bytes per pass:
+ *     7 MB at cfg4) followed by the single-device fixed-order combine on every
+ *     rank: bitwise the single-device result. */
+EDAA_API int edaa_set_shard_exchange(edaa_ctx* ctx, int mode);
 
 /* Order of the pass kernels' (pixel slice, run chunk) work items (no reference
  * counterpart: a scheduling knob of this implementation).  0 = auto (chunk-major

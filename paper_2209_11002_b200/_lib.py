@@ -87,6 +87,7 @@ SIGNATURES = [
     ("edaa_set_pixel_shard", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int]),
     ("edaa_shard_pixels", C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     ("edaa_set_shard_emulation", C.c_int, [C.c_void_p, C.c_int]),
+    ("edaa_set_shard_exchange", C.c_int, [C.c_void_p, C.c_int]),
     ("edaa_set_pass_order", C.c_int, [C.c_void_p, C.c_int]),
     ("edaa_version", C.c_char_p, []),
     ("edaa_max_endmembers", C.c_size_t, []),

@@ -56,7 +56,7 @@ struct edaa_ctx {
   Buf A, Lg, Bv, Y, Z, XAt, AAt, Gbuf, colm, colS, collogS, eta_a, eta_b, gamma, trace, part_C,
       part_m, part_S, part_obj, fac, E, fit, mu, part_fit, seeds, fail_key, fail_code, fail_value, cand,
       selected, fit_min, obsA, pr_b, pr_a, pr_y, pr_r, pr_g, pr_rat, pr_part, pr_out, in_raw, in_x,
-      in_flags, in_bad;
+      in_flags, in_bad, shard_red, shard_stage;
   int fit_blocks = 0;
   // instrumentation
   bool profile = false;
@@ -84,6 +84,7 @@ struct edaa_ctx {
   ncclComm_t comm = nullptr;
   int shard_rank = 0, shard_world = 1;
   int shard_emulate = 0;  // > 1: run the slice ranges of that many ranks one after another here
+  int shard_exchange = 0; // 0: allreduce of the rank-reduced L×Q / Q×Q / 2Q blocks; 1: broadcast of every slice partial (bitwise)
   int pass_order = 0;     // pass item order: 0 auto, 1 chunk-major, 2 slice-major (edaa_set_pass_order)
 };
 
@@ -288,6 +289,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -316,6 +318,7 @@ const NcclApi& nccl() {
     sym(a.CommDestroy, "ncclCommDestroy");
     sym(a.Broadcast, "ncclBroadcast");
     sym(a.AllReduce, "ncclAllReduce");
+    sym(a.AllGather, "ncclAllGather");
     sym(a.GroupStart, "ncclGroupStart");
     sym(a.GroupEnd, "ncclGroupEnd");
     sym(a.GetErrorString, "ncclGetErrorString");
@@ -436,7 +439,30 @@ int make_xmap(edaa_ctx* c, const Dims& d) {
   return EDAA_OK;
 }
 
+// Staging plan of the final state exchange: widest pixel range of a rank, rows per all-gather.
+void state_stage_plan(const edaa_ctx* c, const Dims& d, int* wmax, int* rblk) {
+  const int W = c->shard_world;
+  int w = 1;
+  for (int q = 0; q < W; ++q) {
+    int a = 0, b = 0, j0 = 0, j1 = 0;
+    shard_slices(d, q, W, &a, &b);
+    slice_pixels(d, a, b, &j0, &j1);
+    w = std::max(w, j1 - j0);
+  }
+  const size_t cap = size_t(32) << 20;  // doubles of receive staging (256 MB)
+  *wmax = w;
+  *rblk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(static_cast<size_t>(d.M) * d.p,
+                                                                 cap / (static_cast<size_t>(W) * w))));
+}
+
 int alloc_solve(edaa_ctx* c, const Dims& d, size_t T) {
+  if (c->comm || c->shard_emulate > 1)
+    EDAA_CUDA(c, ensure(c->shard_red, edaa::shard_red_doubles(d) * std::max(1, c->shard_emulate) * 8));
+  if (c->comm) {
+    int wmax = 0, rblk = 0;
+    state_stage_plan(c, d, &wmax, &rblk);
+    EDAA_CUDA(c, ensure(c->shard_stage, static_cast<size_t>(rblk) * wmax * (c->shard_world + 1) * 8));
+  }
   const size_t mpn = static_cast<size_t>(d.M) * d.p * d.Npad * 8;
   const size_t lq = static_cast<size_t>(d.Lpad) * d.Qs * 8;
   const size_t qq = static_cast<size_t>(d.QCpad) * d.Qs * 8;
@@ -630,7 +656,7 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   key.K2 = prm->inner_iters_b;
   key.gen = c->gen;
   key.comm = c->comm;
-  key.emulate = c->shard_emulate;
+  key.emulate = c->shard_emulate * 2 + c->shard_exchange;
   if (!(c->graph_exec && std::memcmp(&key, &c->graph_key, sizeof key) == 0)) {
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     c->graph_exec = nullptr;
@@ -690,24 +716,36 @@ int exchange_partials(edaa_ctx* c, int mode) {
 
 // Before the final phase: every rank's A and logits pixel columns to everyone,
 // and the per-run failure keys (set by the pass of the pixel's owner) min-reduced.
+// A rank's columns are packed into a dense [rows][wmax] block, ONE all-gather per
+// array (and per block of rows, bounded staging) moves them, and every rank's
+// block is unpacked into place (its own too: the values it already holds).
 int exchange_state(edaa_ctx* c) {
   const Dims& d = c->d;
   const NcclApi& n = nccl();
-  EDAA_NCCL(c, n.GroupStart());
+  const int W = c->shard_world;
   EDAA_NCCL(c, n.AllReduce(c->fail_key.p, c->fail_key.p, d.M, ncclUint64, ncclMin, c->comm, c->stream));
-  for (int q = 0; q < c->shard_world; ++q) {
-    int a = 0, b = 0, j0 = 0, j1 = 0;
-    shard_slices(d, q, c->shard_world, &a, &b);
-    slice_pixels(d, a, b, &j0, &j1);
-    if (j1 <= j0) continue;
-    for (int row = 0; row < d.M * d.p; ++row) {
-      double* pa = P<double>(c->A) + static_cast<size_t>(row) * d.Npad + j0;
-      double* pl = P<double>(c->Lg) + static_cast<size_t>(row) * d.Npad + j0;
-      EDAA_NCCL(c, n.Broadcast(pa, pa, j1 - j0, ncclFloat64, q, c->comm, c->stream));
-      EDAA_NCCL(c, n.Broadcast(pl, pl, j1 - j0, ncclFloat64, q, c->comm, c->stream));
+  int wmax = 0, rblk = 0;
+  state_stage_plan(c, d, &wmax, &rblk);
+  const int rows = d.M * d.p;
+  double* send = P<double>(c->shard_stage);
+  double* recv = send + static_cast<size_t>(rblk) * wmax;
+  int mj0 = 0, mj1 = 0;
+  slice_pixels(d, d.sl0, d.sl1, &mj0, &mj1);
+  for (double* arr : {P<double>(c->A), P<double>(c->Lg)}) {
+    for (int r0 = 0; r0 < rows; r0 += rblk) {
+      const int nr = std::min(rblk, rows - r0);
+      double* base = arr + static_cast<size_t>(r0) * d.Npad;
+      EDAA_LAUNCH(c, edaa::launch_pack_cols(base, send, nr, d.Npad, mj0, mj1 - mj0, wmax, false, nullptr, c->stream));
+      EDAA_NCCL(c, n.AllGather(send, recv, static_cast<size_t>(rblk) * wmax, ncclFloat64, c->comm, c->stream));
+      for (int q = 0; q < W; ++q) {
+        int a = 0, b = 0, j0 = 0, j1 = 0;
+        shard_slices(d, q, W, &a, &b);
+        slice_pixels(d, a, b, &j0, &j1);
+        EDAA_LAUNCH(c, edaa::launch_pack_cols(nullptr, recv + static_cast<size_t>(q) * rblk * wmax, nr, d.Npad, j0,
+                                              j1 - j0, wmax, true, base, c->stream));
+      }
     }
   }
-  EDAA_NCCL(c, n.GroupEnd());
   return EDAA_OK;
 }
 
@@ -725,8 +763,63 @@ int run_pass(edaa_ctx* c, int mode, edaa::PassArgs pa) {
     return EDAA_OK;
   }
   const int rc = launch_pass_profiled(c, mode, pa);
-  if (rc || c->comm == nullptr) return rc;
+  if (rc || c->comm == nullptr || c->shard_exchange == 0) return rc;
   return exchange_partials(c, mode);
+}
+
+// The combine of one pass.  Unsharded, or sharded with the broadcast exchange
+// (every slice partial is already on every rank): the fixed-order combine over
+// all slices.  Sharded with the allreduce exchange (the default; BASELINE
+// north_star: "NCCL allreduce of the L×p and p×p partial sums"): every rank
+// reduces the slices it owns into one block of Lrows×Qs + 2·Qs + M doubles, the
+// blocks are combined across ranks — for the B step a max-allreduce of the 
+// column maxima, a rescale to that common reference, then ONE sum-allreduce of
+// C | S | obj — and the same combine kernels finish from the reduced block as
+// if it were a single slice.  Per pass and rank that is ~(L+24)·Q·8 bytes
+// (cfg4 single run: 47.6 KB) instead of nslices·(L+24)·Q·8 (7 MB).  The sum
+// over ranks is NCCL's, so the sharded result equals the single-device one to
+// rounding (not bitwise; the broadcast exchange keeps the bitwise property).
+int combine_pass(edaa_ctx* c, const edaa::CombineArgs& a, int nlaunch) {
+  const Dims& d = c->d;
+  const bool emul = c->shard_emulate > 1;
+  if (c->shard_exchange != 0 || (!c->comm && !emul)) {
+    EDAA_LAUNCH_N(c, edaa::launch_combine(a, c->stream), nlaunch);
+    return EDAA_OK;
+  }
+  const bool lse = a.mode == edaa::kModeB || a.mode == edaa::kModeInit;
+  const size_t blk = edaa::shard_red_doubles(d), nsum = edaa::shard_red_sum_doubles(d);
+  const int world = emul ? c->shard_emulate : 1;
+  double* red = P<double>(c->shard_red);
+  EDAA_CUDA(c, cudaMemsetAsync(red, 0, blk * world * 8, c->stream));
+  double* mg = red + edaa::shard_red_off(d, 4);
+  if (emul) {
+    for (int q = 0; q < world; ++q) {
+      int s0 = 0, s1 = 0;
+      shard_slices(d, q, world, &s0, &s1);
+      EDAA_LAUNCH_N(c, edaa::launch_shard_reduce(a, s0, s1, red + q * blk, c->stream), lse ? 2 : 1);
+    }
+    if (lse) {
+      EDAA_LAUNCH(c, edaa::launch_shard_emul_max(d, red, blk, world, c->stream));
+      for (int q = 0; q < world; ++q) EDAA_LAUNCH(c, edaa::launch_shard_rescale(d, red + q * blk, mg, c->stream));
+    }
+    EDAA_LAUNCH(c, edaa::launch_shard_emul_sum(red, blk, world, nsum, c->stream));
+  } else {
+    const NcclApi& n = nccl();
+    EDAA_LAUNCH_N(c, edaa::launch_shard_reduce(a, d.sl0, d.sl1, red, c->stream), lse ? 2 : 1);
+    if (lse) {
+      EDAA_NCCL(c, n.AllReduce(red + edaa::shard_red_off(d, 3), mg, d.Qs, ncclFloat64, ncclMax, c->comm, c->stream));
+      EDAA_LAUNCH(c, edaa::launch_shard_rescale(d, red, mg, c->stream));
+    }
+    EDAA_NCCL(c, n.AllReduce(red, red, nsum, ncclFloat64, ncclSum, c->comm, c->stream));
+  }
+  edaa::CombineArgs f = a;  // finish from the reduced block: one slice holding everything
+  f.d.nslices = 1;
+  f.part_C = red;
+  f.part_S = red + edaa::shard_red_off(d, 1);
+  f.part_obj = red + edaa::shard_red_off(d, 2);
+  f.part_m = mg;
+  EDAA_LAUNCH_N(c, edaa::launch_combine(f, c->stream), nlaunch);
+  return EDAA_OK;
 }
 
 int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
@@ -757,7 +850,8 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
     edaa::PassArgs pa = pass_args(c, 0, nullptr);
     rc = run_pass(c, edaa::kModeInit, pa);
     if (rc) return rc;
-    EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, 0, edaa::kModeInit, 0), st));
+    rc = combine_pass(c, combine_args(c, 0, edaa::kModeInit, 0), 1);
+    if (rc) return rc;
     EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostInit), st));
   }
   for (size_t t = 1; t <= c->T; ++t) {
@@ -766,7 +860,8 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
     if (hook) pa.observe_A = P<double>(c->obsA);
     rc = run_pass(c, edaa::kModeA, pa);
     if (rc) return rc;
-    EDAA_LAUNCH_N(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeA, ti - 1), st), 2);
+    rc = combine_pass(c, combine_args(c, ti, edaa::kModeA, ti - 1), 2);
+    if (rc) return rc;
     if (hook) {
       // B is fixed through the A block; snapshot it once, then replay the K1 iterates.
       rc = download_b(c, hook);
@@ -787,7 +882,8 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
       edaa::PassArgs pb = pass_args(c, ti, P<double>(c->Z));
       rc = run_pass(c, edaa::kModeB, pb);
       if (rc) return rc;
-      EDAA_LAUNCH(c, edaa::launch_combine(combine_args(c, ti, edaa::kModeB, 0, static_cast<int>(k)), st));
+      rc = combine_pass(c, combine_args(c, ti, edaa::kModeB, 0, static_cast<int>(k)), 1);
+      if (rc) return rc;
       if (k == prm->inner_iters_b) EDAA_LAUNCH(c, edaa::launch_post(post_args(c, edaa::kPostG), st));
       if (hook) {
         rc = download_b(c, hook);
@@ -811,7 +907,8 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
     rc = run_pass(c, edaa::kModeObj, po);
     if (rc) return rc;
     edaa::CombineArgs co = combine_args(c, static_cast<int>(c->T), edaa::kModeObj, static_cast<int>(c->T));
-    EDAA_LAUNCH(c, edaa::launch_combine(co, st));
+    rc = combine_pass(c, co, 1);
+    if (rc) return rc;
     if (c->comm) {
       rc = exchange_state(c);
       if (rc) return rc;
@@ -1243,6 +1340,13 @@ int edaa_set_shard_emulation(edaa_ctx* c, int world) {
   if (!c || world < 0) return EDAA_ERR_INVALID;
   if (c->comm) return set_err(c, EDAA_ERR_STATE, "shard emulation with a live communicator");
   c->shard_emulate = world;
+  ++c->image_gen;
+  return EDAA_OK;
+}
+
+int edaa_set_shard_exchange(edaa_ctx* c, int mode) {
+  if (!c || (mode != 0 && mode != 1)) return EDAA_ERR_INVALID;
+  c->shard_exchange = mode;
   ++c->image_gen;
   return EDAA_OK;
 }

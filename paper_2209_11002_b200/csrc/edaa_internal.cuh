@@ -196,6 +196,16 @@ cudaError_t launch_select(const double* fit, const double* mu, const int* fail_c
                           const unsigned long long* fail_key, int M, double slack,
                           unsigned char* cand, long long* selected, double* fit_min,
                           cudaStream_t st);
+// pixel sharding, allreduce exchange (edaa_kernels.cu): the rank-local block of one pass
+size_t shard_red_doubles(const Dims& d);       // whole block
+size_t shard_red_sum_doubles(const Dims& d);   // its sum-reduced prefix (C | S | obj)
+size_t shard_red_off(const Dims& d, int what); // 0 C, 1 S, 2 obj, 3 m (rank), 4 m (global)
+cudaError_t launch_shard_reduce(const CombineArgs& a, int s0, int s1, double* red, cudaStream_t st);
+cudaError_t launch_shard_rescale(const Dims& d, double* red, const double* m_glob, cudaStream_t st);
+cudaError_t launch_shard_emul_max(const Dims& d, double* red, size_t stride, int world, cudaStream_t st);
+cudaError_t launch_shard_emul_sum(double* red, size_t stride, int world, size_t n, cudaStream_t st);
+cudaError_t launch_pack_cols(const double* src, double* stage, int rows, int Npad, int j0, int w, int wmax,
+                             bool unpack, double* dst, cudaStream_t st);
 size_t pass_smem_bytes(const Dims& d, int nbuf);
 // primitives (edaa_prims.cu)
 cudaError_t launch_residual(const void* X, int xbytes, const double* Y, const double* A, double* R,

@@ -736,6 +736,151 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Pixel sharding, allreduce exchange (north_star: "NCCL allreduce of the L×p and
+// p×p partial sums").  Each rank reduces the partials of the slices it owns into
+// ONE block of Lrows×Qs (+ 2·Qs + M) doubles, the blocks are summed across ranks
+// (log-sum-exp aware for the B step: column maxima first), and the unchanged
+// combine kernels finish from the reduced block as if it were a single slice.
+//   block layout (doubles): C [Lrows][Qs] | S [Qs] | obj [M] | m [Qs] | m_glob [Qs]
+__host__ __device__ inline size_t red_off_S(const Dims& d) { return static_cast<size_t>(d.Lrows) * d.Qs; }
+__host__ __device__ inline size_t red_off_obj(const Dims& d) { return red_off_S(d) + d.Qs; }
+__host__ __device__ inline size_t red_off_m(const Dims& d) { return red_off_obj(d) + d.M; }
+__host__ __device__ inline size_t red_off_mg(const Dims& d) { return red_off_m(d) + d.Qs; }
+
+// B / init: per column, the max m_r of the owned slices' maxima, the rescale
+// factors e^{m_s − m_r} (into ca.fac) and S_r = Σ_s S_s·e^{m_s − m_r}.  One warp
+// per column, lanes stride the slices, fixed xor tree.
+__global__ void k_shard_colmax(CombineArgs ca, int s0, int s1, double* red) {
+  const Dims& d = ca.d;
+  const int col = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (col >= d.Qs) return;
+  double m = -INFINITY;
+  for (int sl = s0 + lane; sl < s1; sl += 32) m = fmax(m, ca.part_m[static_cast<size_t>(sl) * d.Qs + col]);
+  m = warp_max(m);
+  double S = 0.0;
+  for (int sl = s0 + lane; sl < s1; sl += 32) {
+    const double ms = ca.part_m[static_cast<size_t>(sl) * d.Qs + col];
+    const double f = (ms == -INFINITY) ? 0.0 : exp(ms - m);
+    ca.fac[static_cast<size_t>(sl) * d.Qs + col] = f;
+    S += ca.part_S[static_cast<size_t>(sl) * d.Qs + col] * f;
+  }
+  S = warp_sum(S);
+  if (lane == 0) {
+    red[red_off_m(d) + col] = m;
+    red[red_off_S(d) + col] = S;
+  }
+}
+
+// Rows of the block: Σ_s C_s (A) or Σ_s C_s·e^{m_s − m_r} (B / init), slices in
+// ascending order; block (0,0) also folds the owned slices' objective terms.
+__global__ void k_shard_rowsum(CombineArgs ca, int s0, int s1, int rows, double* red) {
+  const Dims& d = ca.d;
+  const bool lse = ca.mode == kModeB || ca.mode == kModeInit;
+  if (!lse && blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int r = threadIdx.y * 32 + threadIdx.x; r < d.M; r += 256) {
+      double o = 0.0;
+      for (int sl = s0; sl < s1; ++sl) o += ca.part_obj[static_cast<size_t>(sl) * d.M + r];
+      red[red_off_obj(d) + r] = o;
+    }
+  }
+  const int col = blockIdx.x * 32 + threadIdx.x;
+  const int row = blockIdx.y * 8 + threadIdx.y;
+  if (col >= d.Qs || row >= rows) return;
+  const double* src = ca.part_C + static_cast<size_t>(row) * d.Qs + col;
+  const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
+  double s = 0.0;
+  if (lse) {
+    for (int sl = s0; sl < s1; ++sl) s += src[sl * sstride] * ca.fac[static_cast<size_t>(sl) * d.Qs + col];
+  } else {
+    for (int sl = s0; sl < s1; ++sl) s += src[sl * sstride];
+  }
+  red[static_cast<size_t>(row) * d.Qs + col] = s;
+}
+
+// B / init, after the column maxima were max-reduced across ranks: bring the
+// rank's block to the common reference, C ← C·e^{m_r − m}, S ← S·e^{m_r − m}.
+__global__ void k_shard_rescale(Dims d, double* red, const double* m_glob) {
+  const int col = blockIdx.x * 32 + threadIdx.x;
+  if (col >= d.Qs) return;
+  const double mr = red[red_off_m(d) + col], mg = m_glob[col];
+  const double f = (mr == -INFINITY) ? 0.0 : exp(mr - mg);
+  for (int row = blockIdx.y * 8 + threadIdx.y; row < d.Lpad; row += gridDim.y * 8)
+    red[static_cast<size_t>(row) * d.Qs + col] *= f;
+  if (blockIdx.y == 0 && threadIdx.y == 0) red[red_off_S(d) + col] *= f;
+}
+
+// One-device emulation of the two collectives (tests): blocks of `world` ranks
+// `stride` doubles apart; the max of their m into block 0's m_glob, and the sum
+// of their first `n` doubles, in rank order, into block 0.
+__global__ void k_shard_emul_max(Dims d, double* red, size_t stride, int world) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= d.Qs) return;
+  double m = -INFINITY;
+  for (int q = 0; q < world; ++q) m = fmax(m, red[q * stride + red_off_m(d) + col]);
+  red[red_off_mg(d) + col] = m;
+}
+__global__ void k_shard_emul_sum(double* red, size_t stride, int world, size_t n) {
+  const size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = red[e];
+  for (int q = 1; q < world; ++q) s += red[q * stride + e];
+  red[e] = s;
+}
+
+// Final state exchange: a rank's pixel columns [j0, j0+w) of a [rows][Npad] array
+// to / from a dense [rows][wmax] staging block (one all-gather per array).
+__global__ void k_pack_cols(const double* src, double* stage, int rows, int Npad, int j0, int w, int wmax) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= w) return;
+  for (int r = blockIdx.y; r < rows; r += gridDim.y)
+    stage[static_cast<size_t>(r) * wmax + j] = src[static_cast<size_t>(r) * Npad + j0 + j];
+}
+__global__ void k_unpack_cols(double* dst, const double* stage, int rows, int Npad, int j0, int w, int wmax) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= w) return;
+  for (int r = blockIdx.y; r < rows; r += gridDim.y)
+    dst[static_cast<size_t>(r) * Npad + j0 + j] = stage[static_cast<size_t>(r) * wmax + j];
+}
+
+size_t shard_red_doubles(const Dims& d) { return red_off_mg(d) + d.Qs; }
+size_t shard_red_sum_doubles(const Dims& d) { return red_off_m(d); }
+size_t shard_red_off(const Dims& d, int what) {
+  return what == 0 ? 0 : what == 1 ? red_off_S(d) : what == 2 ? red_off_obj(d) : what == 3 ? red_off_m(d) : red_off_mg(d);
+}
+
+cudaError_t launch_shard_reduce(const CombineArgs& a, int s0, int s1, double* red, cudaStream_t st) {
+  const Dims& d = a.d;
+  const bool lse = a.mode == kModeB || a.mode == kModeInit;
+  if (lse) k_shard_colmax<<<(d.Qs + 7) / 8, 256, 0, st>>>(a, s0, s1, red);
+  const int rows = a.mode == kModeObj ? 0 : (lse ? d.Lpad : d.Lrows);
+  k_shard_rowsum<<<dim3((d.Qs + 31) / 32, std::max(1, (rows + 7) / 8)), dim3(32, 8), 0, st>>>(a, s0, s1, rows, red);
+  return cudaGetLastError();
+}
+cudaError_t launch_shard_rescale(const Dims& d, double* red, const double* m_glob, cudaStream_t st) {
+  k_shard_rescale<<<dim3((d.Qs + 31) / 32, std::min(32, (d.Lpad + 7) / 8)), dim3(32, 8), 0, st>>>(d, red, m_glob);
+  return cudaGetLastError();
+}
+cudaError_t launch_shard_emul_max(const Dims& d, double* red, size_t stride, int world, cudaStream_t st) {
+  k_shard_emul_max<<<(d.Qs + 127) / 128, 128, 0, st>>>(d, red, stride, world);
+  return cudaGetLastError();
+}
+cudaError_t launch_shard_emul_sum(double* red, size_t stride, int world, size_t n, cudaStream_t st) {
+  k_shard_emul_sum<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(red, stride, world, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_pack_cols(const double* src, double* stage, int rows, int Npad, int j0, int w, int wmax,
+                             bool unpack, double* dst, cudaStream_t st) {
+  if (w <= 0 || rows <= 0) return cudaSuccess;
+  const dim3 grid((w + 255) / 256, std::min(rows, 1024));
+  if (unpack)
+    k_unpack_cols<<<grid, 256, 0, st>>>(dst, stage, rows, Npad, j0, w, wmax);
+  else
+    k_pack_cols<<<grid, 256, 0, st>>>(src, stage, rows, Npad, j0, w, wmax);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_post(const PostArgs& a, cudaStream_t st) {
   if (a.mode == kPostG)
     launch_pdl(a.d.pdl != 0, k_gram, dim3(a.d.M), dim3(256), 0, st, a);

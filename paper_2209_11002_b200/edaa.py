@@ -383,6 +383,11 @@ class Device:
         device (the sharded decomposition without a collective); 0 or 1 turns it off."""
         self._check(self.lib.edaa_set_shard_emulation(self.h, int(world)))
 
+    def set_shard_exchange(self, mode: int):
+        """Per-pass exchange of a pixel-sharded solve: 0 allreduce of the rank-reduced L×Q / Q×Q /
+        2Q blocks (default, north_star), 1 broadcast of every slice partial (bitwise)."""
+        self._check(self.lib.edaa_set_shard_exchange(self.h, int(mode)))
+
     def set_pass_order(self, order: int):
         """Pass work-item order: 0 auto, 1 chunk-major, 2 slice-major, 3 interleaved (results are
         bitwise identical; include/edaa_b200.h)."""

@@ -299,43 +299,79 @@ def _solve_all(d, x, p, T, seeds, gammas):
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_pixel_sharded_decomposition_is_bitwise_the_single_device_solve(world):
     """The pixel-sharded schedule (§8e) on one device: every pass launched as
-    `world` slice-range launches, exactly the work split the ranks do.  The fixed
-    slice order makes it bitwise equal to the unsharded solve."""
+    `world` slice-range launches, exactly the work split the ranks do.  With the
+    BROADCAST exchange (every slice partial on every rank, then the fixed-order
+    combine) it is bitwise equal to the unsharded solve."""
     x = synth.small_scene(41, 4000, 4, seed=5)
     cfg = edaa.EnsembleConfig(runs=7, solver=edaa.SolverConfig(endmembers=4, outer_iters=8))
     seeds, gammas = edaa.ensemble_plan(cfg)
     d = dev()
     base = _solve_all(d, x, 4, 8, seeds, gammas)
     d.set_shard_emulation(world)
+    d.set_shard_exchange(1)
     try:
         got = _solve_all(d, x, 4, 8, seeds, gammas)
     finally:
         d.set_shard_emulation(0)
+        d.set_shard_exchange(0)
     for u, v in zip(base[0], got[0]):
         assert all(np.array_equal(a, b) for a, b in zip(u, v))
     assert np.array_equal(base[1], got[1]) and base[2] == got[2]
 
 
-def test_pixel_shard_nccl_exchange_runs_inside_the_solve():
-    """A real NCCL communicator (one rank on this one GPU): the partial
-    exchanges after every pass and the final state exchange run inside the
-    captured schedule and leave the result bitwise unchanged."""
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("shape", [(41, 4000, 4, 7), (24, 3000, 12, 3), (30, 777, 3, 1)])
+def test_pixel_sharded_allreduce_exchange_matches_the_single_device_solve(world, shape):
+    """The ALLREDUCE exchange (the default; north_star's "allreduce of the L×p and
+    p×p partial sums"): every emulated rank reduces its own slices to one L×Q / Q×Q /
+    2Q block, the blocks are combined (column maxima, rescale, sum in rank order —
+    what NCCL's max- and sum-allreduce do across GPUs) and the combine finishes
+    from the reduced block.  Same result as the unsharded solve to rounding: the
+    bars of the parity tests, and a 1e-9 guard, on every run of the batch."""
+    L, N, p, M = shape
+    x = synth.small_scene(L, N, p, seed=5)
+    cfg = edaa.EnsembleConfig(runs=M, solver=edaa.SolverConfig(endmembers=p, outer_iters=8))
+    seeds, gammas = edaa.ensemble_plan(cfg)
+    d = dev()
+    base = _solve_all(d, x, p, 8, seeds, gammas)
+    d.set_shard_emulation(world)
+    try:
+        got = _solve_all(d, x, p, 8, seeds, gammas)
+    finally:
+        d.set_shard_emulation(0)
+    for (A0, B0, E0), (A1, B1, E1) in zip(base[0], got[0]):
+        assert np.abs(A0 - A1).max() <= GUARD and np.abs(B0 - B1).max() <= GUARD
+        assert np.abs(E0 - E1).max() <= GUARD
+    assert np.abs(base[1] - got[1]).max() <= GUARD * np.abs(base[1]).max()
+    assert np.allclose(base[2], got[2], rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("exchange", [0, 1])
+def test_pixel_shard_nccl_exchange_runs_inside_the_solve(exchange):
+    """A real NCCL communicator (one rank on this one GPU): the per-pass exchange
+    (0: max- and sum-allreduce of the reduced block; 1: broadcasts of the slice
+    partials) and the final state exchange (pack, all-gather, unpack) run inside
+    the captured schedule; the broadcast exchange leaves the result bitwise
+    unchanged, the allreduce exchange equal to rounding."""
     x = synth.small_scene(30, 3000, 3, seed=2)
     cfg = edaa.SolverConfig(endmembers=3, outer_iters=10, gamma=4.0, seed=11)
     ref = edaa.run(x, cfg)
     d = dev()
+    same = np.array_equal if exchange == 1 else (lambda a, b: np.abs(a - b).max() <= GUARD * max(1.0, np.abs(b).max()))
     try:
+        d.set_shard_exchange(exchange)
         d.set_pixel_shard(d.nccl_unique_id(), 0, 1)
         d.set_image(x)
         for _ in range(2):  # capture, then replay of the graph holding the NCCL calls
             d.solve(3, 10, 5, 5, [cfg.seed], [cfg.gamma])
             A, B, E = d.factors(0)
-            assert np.array_equal(A, ref.abundances) and np.array_equal(B, ref.contributions)
-            assert np.array_equal(E, ref.endmembers)
-            assert np.array_equal(d.traces()[0], ref.objective_trace)
+            assert same(A, ref.abundances) and same(B, ref.contributions)
+            assert same(E, ref.endmembers)
+            assert same(d.traces()[0], ref.objective_trace)
         assert d.shard_pixels() == (0, 3000)
     finally:
         d.set_pixel_shard(None, 0, 1)
+        d.set_shard_exchange(0)
 
 
 def test_pixel_sharded_run_through_torch_distributed_world1():
@@ -353,8 +389,8 @@ def test_pixel_sharded_run_through_torch_distributed_world1():
         cfg = edaa.SolverConfig(endmembers=3, outer_iters=6, gamma=2.0, seed=4)
         got = distributed.run_pixel_sharded(x, cfg)
         ref = edaa.run(x, cfg)
-        assert np.array_equal(got.abundances, ref.abundances)
-        assert np.array_equal(got.objective_trace, ref.objective_trace)
+        assert np.abs(got.abundances - ref.abundances).max() <= GUARD
+        assert np.abs(got.objective_trace - ref.objective_trace).max() <= GUARD * np.abs(ref.objective_trace).max()
     finally:
         dist.destroy_process_group()
 
