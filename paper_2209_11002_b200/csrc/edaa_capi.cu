@@ -21,11 +21,28 @@
 #include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX 3: ranges per solve phase (visible to nsys / ncu --nvtx)
 
 #include "../../include/edaa_b200.h"
 #include "edaa_device.cuh"
 
 using edaa::Dims;
+
+namespace {
+// NVTX range of one schedule phase ("edaa/solve", "edaa/init", "edaa/A t=3", …): marks
+// the host enqueue (and, outside a captured graph, brackets the phase's launches).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* what, size_t t) {
+    char buf[48];
+    std::snprintf(buf, sizeof buf, "edaa/%s t=%zu", what, t);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 struct GraphKey {
   Dims d;
@@ -632,6 +649,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook);
 // schedule (≈ 3 + T·(3 + 4·K2) + 7 kernels) runs — replayed from a CUDA graph
 // captured on the first solve of a given shape (EDAA_NO_GRAPH=1 disables).
 int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
+  NvtxRange nv("edaa/solve");
   Dims d{};
   int rc = make_dims(c, prm, &d);
   if (rc) return rc;
@@ -847,6 +865,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
 
   // ---- initialisation: B⁰, Y⁰ = X·B⁰, η, G ----
   {
+    NvtxRange nv("edaa/init");
     edaa::PassArgs pa = pass_args(c, 0, nullptr);
     rc = run_pass(c, edaa::kModeInit, pa);
     if (rc) return rc;
@@ -856,6 +875,9 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
   }
   for (size_t t = 1; t <= c->T; ++t) {
     const int ti = static_cast<int>(t);
+    NvtxRange nv_outer("outer", t);
+    {
+    NvtxRange nv_a("edaa/A block");
     edaa::PassArgs pa = pass_args(c, ti, P<double>(c->Y));
     if (hook) pa.observe_A = P<double>(c->obsA);
     rc = run_pass(c, edaa::kModeA, pa);
@@ -878,6 +900,8 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
                  d.p, d.N, hook->user);
       }
     }
+    }
+    NvtxRange nv_b("edaa/B block");
     for (size_t k = 1; k <= prm->inner_iters_b; ++k) {
       edaa::PassArgs pb = pass_args(c, ti, P<double>(c->Z));
       rc = run_pass(c, edaa::kModeB, pb);
@@ -903,6 +927,7 @@ int enqueue_solve(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) 
   }
   // ---- finalisation: trace[T], B̂, Ê = X·B̂, fit, coherence ----
   {
+    NvtxRange nv("edaa/final");
     edaa::PassArgs po = pass_args(c, static_cast<int>(c->T), P<double>(c->Y));
     rc = run_pass(c, edaa::kModeObj, po);
     if (rc) return rc;

@@ -686,3 +686,29 @@ def test_cfg4_full_size_runs_match_reference():
         assert np.abs(B[cols, :] - g["B_rows"]).max() <= GUARD
         assert np.abs(A.sum(axis=1) - g["A_rowsum"]).max() <= 1e-6 * x.shape[1]
         assert np.abs(B.max(axis=0) - g["B_colmax"]).max() <= GUARD
+
+
+@pytest.mark.parametrize("L,N,p,M", [(41, 4000, 4, 13), (24, 3000, 12, 3), (33, 700, 7, 5)])
+def test_repeated_solves_are_bitwise_identical_stress(L, N, p, M):
+    """Race evidence without compute-sanitizer (closed on this GPU pool,
+    profiles/round2/sanitizer_refused.txt): the pass kernels' mbarrier / named-
+    barrier pipeline hands tiles between warp groups through shared memory, so a
+    hand-off race shows up as run-to-run differences.  Twelve solves of a
+    multi-chunk, multi-slice batch, alternating with a different shape in between
+    (so buffers and the captured graph are re-established), must agree bit for bit."""
+    x = synth.small_scene(L, N, p, seed=5)
+    other = synth.small_scene(20, 900, 3, seed=1)
+    cfg = edaa.EnsembleConfig(runs=M, solver=edaa.SolverConfig(endmembers=p, outer_iters=6))
+    seeds, gammas = edaa.ensemble_plan(cfg)
+    d = dev()
+    first = None
+    for rep in range(12):
+        if rep % 4 == 3:
+            _solve_all(d, other, 3, 2, [1, 2], [1.0, 8.0])
+        got = _solve_all(d, x, p, 6, seeds, gammas)
+        if first is None:
+            first = got
+            continue
+        for u, v in zip(first[0], got[0]):
+            assert all(np.array_equal(a, b) for a, b in zip(u, v)), rep
+        assert np.array_equal(first[1], got[1]) and first[2] == got[2], rep
