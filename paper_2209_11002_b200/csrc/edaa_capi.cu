@@ -10,6 +10,7 @@
 //   objective pass (trace[T]) → combine; materialise B; E = X·B (reference
 //   order); fit_l1; coherence.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -122,7 +123,7 @@ int cuda_fail(edaa_ctx* c, cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #call); \
   } while (0)
 
-uint64_t g_realloc_count = 0;  // any device (re)allocation invalidates captured graphs
+std::atomic<uint64_t> g_realloc_count{0};  // any device (re)allocation invalidates captured graphs (contexts on several host threads)
 
 cudaError_t ensure(edaa_ctx::Buf& b, size_t bytes) {
   if (b.cap >= bytes && b.p) return cudaSuccess;
@@ -662,7 +663,7 @@ int solve_impl(edaa_ctx* c, const edaa_solve_params* prm, ObserveHook* hook) {
   if (rc) return rc;
   rc = make_xmap(c, d);
   if (rc) return rc;
-  c->gen = g_realloc_count * 1000003ull + c->image_gen;
+  c->gen = g_realloc_count.load() * 1000003ull + c->image_gen;
   cudaStream_t st = c->stream;
   EDAA_CUDA(c, cudaMemcpyAsync(c->seeds.p, prm->seeds, d.M * 8, cudaMemcpyHostToDevice, st));
   EDAA_CUDA(c, cudaMemcpyAsync(c->gamma.p, prm->gammas, d.M * 8, cudaMemcpyHostToDevice, st));

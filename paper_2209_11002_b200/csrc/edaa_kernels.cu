@@ -719,13 +719,10 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
     return cudaGetLastError();
   }
   if (a.mode != kModeA) {  // B step / init: normalisers, Y and Z in one kernel
-    static bool attr = false;
-    if (!attr) {
-      const cudaError_t ea = cudaFuncSetAttribute(k_combine_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  kMaxSlices * kQMax * static_cast<int>(sizeof(double)));
-      if (ea != cudaSuccess) return ea;
-      attr = true;
-    }
+    // a constant, set on whichever device is current (per-device, per-function state)
+    const cudaError_t ea = cudaFuncSetAttribute(k_combine_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                kMaxSlices * kQMax * static_cast<int>(sizeof(double)));
+    if (ea != cudaSuccess) return ea;
     return launch_pdl(d.pdl != 0, k_combine_b, dim3(d.NCH, (d.Lpad + kBR - 1) / kBR), dim3(256),
                       static_cast<size_t>(d.nslices) * kQMax * sizeof(double), st, a);
   }

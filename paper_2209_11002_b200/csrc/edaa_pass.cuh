@@ -942,8 +942,10 @@ cudaError_t launch_pass_ctf(const PassArgs& a, cudaStream_t st, int pt) {
     }
     if (kern == nullptr) return cudaErrorInvalidValue;
   }
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  // Always the device maximum, never this launch's size: the attribute is per-function
+  // state shared by every context on the device, so two host threads solving different
+  // batches concurrently would otherwise lower it under each other's launches.
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   if (e != cudaSuccess) return e;
   e = launch_pdl(a.d.pdl != 0, kern, grid, dim3(kThreads), smem, st, a, *static_cast<const CUtensorMap*>(a.xmap));
   if (e != cudaSuccess) return e;

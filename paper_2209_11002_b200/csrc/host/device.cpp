@@ -1,5 +1,6 @@
 #include "device.hpp"
 
+#include <algorithm>
 #include <cstdlib>
 #include <memory>
 #include <vector>
@@ -33,6 +34,21 @@ int device_count() {
       d->ordinal = static_cast<int>(r.devices.size());
       if (edaa_create(d->ordinal, &d->ctx) != EDAA_OK) break;
       r.devices.push_back(std::move(d));
+    }
+    // EDAA_VIRTUAL_DEVICES=K (K > visible GPUs): K contexts placed round-robin on
+    // the visible GPUs, each with its own stream and buffers.  run_ensemble then
+    // takes its multi-device branch (one host thread and one shard of the runs
+    // per context, host-side select_runs) on a single GPU — how the tests cover
+    // that branch on a one-GPU box.
+    if (const char* env = std::getenv("EDAA_VIRTUAL_DEVICES")) {
+      const int real = static_cast<int>(r.devices.size());
+      const int want = std::min(64, std::atoi(env));
+      while (real > 0 && static_cast<int>(r.devices.size()) < want) {
+        auto d = std::make_unique<Device>();
+        d->ordinal = static_cast<int>(r.devices.size());
+        if (edaa_create(d->ordinal % real, &d->ctx) != EDAA_OK) break;
+        r.devices.push_back(std::move(d));
+      }
     }
     r.count = static_cast<int>(r.devices.size());
   }

@@ -167,3 +167,34 @@ def test_cli_device_ingest_equals_host_normalisation(tmp_path, dtype):
     for host in (False, True):
         r = unmix(str(tmp_path / "z.hdr"), str(tmp_path / "o"), host=host)
         assert r.returncode == 2 and "degenerate input: all pixels are zero" in r.stderr, r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", [2, 3])
+def test_multi_device_run_ensemble_equals_single_device(tmp_path, devices):
+    """run_ensemble's multi-device branch (csrc/host/ensemble.cpp: one host thread
+    and one contiguous shard of the runs per device context, records merged, the
+    host select_runs, factors fetched from the owner) — the GPU analogue of the
+    reference's worker-count determinism (ensemble.cpp:141-162,
+    test_ensemble.cpp:118-148).  EDAA_VIRTUAL_DEVICES places that many contexts on
+    this one GPU; the bundle must equal the single-context one byte for byte
+    (a run's arithmetic does not depend on its batch), but for wall_ms."""
+    import json
+    run = lambda env, *a: subprocess.run([CLI_BIN, *map(str, a)], capture_output=True, text=True, timeout=300,
+                                         env=dict(os.environ, **env))
+    s = run({}, "synth", "--bands", 20, "--pixels", 900, "--endmembers", 4, "--snr", 35, "--seed", 9,
+            "--output", tmp_path / "fx")
+    assert s.returncode == 0, s.stderr
+    outs = {}
+    for name, env in (("one", {}), ("many", {"EDAA_VIRTUAL_DEVICES": str(devices)})):
+        u = run(env, "unmix", "--input", tmp_path / "fx" / "cube.npy", "--endmembers", 4, "--runs", 11,
+                "--outer", 25, "--output", tmp_path / name, "--json")
+        assert u.returncode == 0, u.stderr
+        outs[name] = json.loads(u.stdout)
+    for f in ("abundances.npy", "endmembers.csv"):
+        assert (tmp_path / "one" / f).read_bytes() == (tmp_path / "many" / f).read_bytes(), f
+    for rep in outs.values():
+        for r in rep["runs"]:
+            r.pop("wall_ms")
+    assert outs["one"] == outs["many"]
+    assert len(outs["one"]["runs"]) == 11

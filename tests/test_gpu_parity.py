@@ -712,3 +712,33 @@ def test_repeated_solves_are_bitwise_identical_stress(L, N, p, M):
         for u, v in zip(first[0], got[0]):
             assert all(np.array_equal(a, b) for a, b in zip(u, v)), rep
         assert np.array_equal(first[1], got[1]) and first[2] == got[2], rep
+
+
+def test_two_contexts_solve_concurrently_from_two_threads():
+    """Two contexts on one device driven by two host threads whose FIRST solves run
+    concurrently (different batch sizes, so different shared-memory plans of the
+    same pass kernels): regression test for a launch failure ("invalid argument")
+    when each thread set the kernels' dynamic-shared-memory attribute to its own
+    size.  Results equal the sequential ones bit for bit."""
+    import threading
+    x = synth.small_scene(20, 900, 4, seed=9)
+    jobs = [([0, 1, 2, 3, 4], [1.0] * 5), ([5, 6, 7, 8, 9, 10], [2.0] * 6)]
+    want = []
+    d = dev()
+    for seeds, gammas in jobs:
+        want.append(_solve_all(d, x, 4, 12, seeds, gammas)[1].copy())
+    ctxs = [edaa.Device(0), edaa.Device(0)]
+    got, errs = [None, None], []
+
+    def work(k):
+        try:
+            got[k] = _solve_all(ctxs[k], x, 4, 12, *jobs[k])[1].copy()
+        except Exception as exc:  # noqa: BLE001
+            errs.append(exc)
+
+    for _ in range(2):
+        th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+        [t.start() for t in th]
+        [t.join() for t in th]
+        assert not errs, errs
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
