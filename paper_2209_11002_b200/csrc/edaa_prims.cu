@@ -93,34 +93,84 @@ __global__ void k_grad_b(const XT* X, const double* rat, double* G, int L, int N
   }
 }
 
-// estimate_abundances (solver.cpp:240-259), one pixel per thread.
-template <class XT>
+// estimate_abundances (solver.cpp:240-259), one pixel per thread, E staged in shared
+// memory; two forms of the step direction −∇ = Eᵀ(x − E·a):
+//   FAST (default): the solver's A-pass form P − G·a with P = Eᵀx_j (one L×p
+//     product per pixel, once) and G = EᵀE (p×p, once per block): an iteration
+//     costs p² instead of 2·L·p multiply-adds, and the entropic
+//     step is the solver's multiplicative softmax a ← max(a, 1e-30)·e^{u − max u}/Σ;
+//   strict (EDAA_ESTIMATE_STRICT=1): the reference's explicit residual in its
+//     operation order (separate multiply and add, log + exp).
+// Both agree with the compiled reference to ≤ 1e-10 for contractive steps
+// (η ≤ 1/λ_max(EᵀE)); for larger η the map is chaotic and ANY reordering —
+// including the strict kernel's libm — drifts (measured at η = 0.5 on the
+// unnormalised cfg3 endmembers: O(1) for both after 100 steps).
+template <class XT, bool FAST>
 __global__ void k_estimate(const XT* X, const double* E, double* A, int L, int N, int Npad, int p,
                            int iters, double eta) {
+  extern __shared__ double es[];  // E [L][p], then G [p][p] (FAST)
+  double* gsm = es + L * p;
+  for (int e = threadIdx.x; e < L * p; e += blockDim.x) es[e] = E[e];
+  __syncthreads();
+  if (FAST) {
+    for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+      const int i = e / p, m = e % p;
+      double s = 0.0;
+      for (int l = 0; l < L; ++l) s = fma(es[l * p + i], es[l * p + m], s);
+      gsm[e] = s;
+    }
+    __syncthreads();
+  }
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
   double a[kMaxP], g[kMaxP];
   for (int i = 0; i < p; ++i) a[i] = 1.0 / static_cast<double>(p);
-  for (int it = 0; it < iters; ++it) {
-    for (int i = 0; i < p; ++i) g[i] = 0.0;
+  if (FAST) {
+    double P[kMaxP];
+    for (int i = 0; i < p; ++i) P[i] = 0.0;
     for (int l = 0; l < L; ++l) {
-      double rec = 0.0;
-      for (int i = 0; i < p; ++i) rec = __dadd_rn(rec, __dmul_rn(E[l * p + i], a[i]));
-      const double r = __dsub_rn(static_cast<double>(X[static_cast<size_t>(l) * Npad + j]), rec);
-      for (int i = 0; i < p; ++i) g[i] = __dadd_rn(g[i], __dmul_rn(E[l * p + i], r));
+      const double x = static_cast<double>(X[static_cast<size_t>(l) * Npad + j]);
+      for (int i = 0; i < p; ++i) P[i] = fma(es[l * p + i], x, P[i]);
     }
-    double top = -INFINITY;
-    for (int i = 0; i < p; ++i) {
-      const double z = (a[i] < kLogFloorValue) ? kLogFloorValue : a[i];
-      g[i] = __dadd_rn(log(z), __dmul_rn(g[i], eta));  // log z + η·(−∇)
-      top = max_like_std(top, g[i]);
+    for (int it = 0; it < iters; ++it) {
+      double top = -INFINITY;
+      for (int i = 0; i < p; ++i) {
+        double ga = 0.0;
+        for (int m = 0; m < p; ++m) ga = fma(gsm[i * p + m], a[m], ga);
+        g[i] = (P[i] - ga) * eta;
+        top = fmax(top, g[i]);
+      }
+      double total = 0.0;
+      for (int i = 0; i < p; ++i) {
+        const double z = (a[i] < kLogFloorValue) ? kLogFloorValue : a[i];
+        g[i] = z * exp(g[i] - top);
+        total += g[i];
+      }
+      for (int i = 0; i < p; ++i) a[i] = g[i] / total;
     }
-    double total = 0.0;
-    for (int i = 0; i < p; ++i) {
-      g[i] = exp(g[i] - top);
-      total = __dadd_rn(total, g[i]);
+  } else {
+    for (int it = 0; it < iters; ++it) {
+      for (int i = 0; i < p; ++i) g[i] = 0.0;
+      for (int l = 0; l < L; ++l) {
+        const double* el = es + l * p;
+        double rec = 0.0;
+        for (int i = 0; i < p; ++i) rec = __dadd_rn(rec, __dmul_rn(el[i], a[i]));
+        const double r = __dsub_rn(static_cast<double>(X[static_cast<size_t>(l) * Npad + j]), rec);
+        for (int i = 0; i < p; ++i) g[i] = __dadd_rn(g[i], __dmul_rn(el[i], r));
+      }
+      double top = -INFINITY;
+      for (int i = 0; i < p; ++i) {
+        const double z = (a[i] < kLogFloorValue) ? kLogFloorValue : a[i];
+        g[i] = __dadd_rn(log(z), __dmul_rn(g[i], eta));  // log z + η·(−∇)
+        top = max_like_std(top, g[i]);
+      }
+      double total = 0.0;
+      for (int i = 0; i < p; ++i) {
+        g[i] = exp(g[i] - top);
+        total = __dadd_rn(total, g[i]);
+      }
+      for (int i = 0; i < p; ++i) a[i] = g[i] / total;
     }
-    for (int i = 0; i < p; ++i) a[i] = g[i] / total;
   }
   for (int i = 0; i < p; ++i) A[static_cast<size_t>(i) * N + j] = a[i];
 }
@@ -191,13 +241,24 @@ cudaError_t launch_check_iterate(const double* m, int rows, int cols, unsigned l
   return cudaGetLastError();
 }
 
+template <class XT>
+static cudaError_t launch_estimate_t(const XT* X, const double* E, double* A, int L, int N, int Npad, int p,
+                                     int iters, double eta, cudaStream_t st) {
+  static const bool strict = [] {
+    const char* v = std::getenv("EDAA_ESTIMATE_STRICT");
+    return v && v[0] == '1';
+  }();
+  const size_t smem = (static_cast<size_t>(L) * p + static_cast<size_t>(p) * p) * sizeof(double);
+  auto kern = strict ? k_estimate<XT, false> : k_estimate<XT, true>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  kern<<<(N + 127) / 128, 128, smem, st>>>(X, E, A, L, N, Npad, p, iters, eta);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_estimate(const void* X, int xbytes, const double* E, double* A, int L, int N,
                             int Npad, int p, int iters, double eta, cudaStream_t st) {
-  if (xbytes == 8)
-    k_estimate<<<(N + 127) / 128, 128, 0, st>>>(static_cast<const double*>(X), E, A, L, N, Npad, p, iters, eta);
-  else
-    k_estimate<<<(N + 127) / 128, 128, 0, st>>>(static_cast<const float*>(X), E, A, L, N, Npad, p, iters, eta);
-  return cudaGetLastError();
+  return xbytes == 8 ? launch_estimate_t(static_cast<const double*>(X), E, A, L, N, Npad, p, iters, eta, st)
+                     : launch_estimate_t(static_cast<const float*>(X), E, A, L, N, Npad, p, iters, eta, st);
 }
 
 }  // namespace edaa
