@@ -68,6 +68,33 @@ struct LanesPerPixel {
   static constexpr int value = PT <= 4 ? 1 : (PT <= 12 ? 2 : 4);
 };
 
+// check_iterate (solver.cpp:65-90) on one pixel's column held by TPP lanes (EPT
+// entries each, `ownbits` the valid ones), evaluated exactly and in the
+// reference's scan order; posts the first failing check to the run's key.  Out of
+// line: it is reached only when the update's range test on Σ fires, and must not
+// cost the K1 loop registers.  All lanes of the pixel's group call it together.
+template <int EPT, int TPP>
+__device__ __noinline__ void post_simplex_failure(unsigned long long* slot, unsigned tb, int k, int pix, int e0,
+                                                  unsigned gmask, const double* a, unsigned ownbits) {
+  double csum = 0.0;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e)
+    if (ownbits >> e & 1u) csum += a[e];
+#pragma unroll
+  for (int o = 1; o < TPP; o <<= 1) csum += __shfl_xor_sync(gmask, csum, o);
+  unsigned long long key = ~0ull;
+#pragma unroll
+  for (int e = EPT - 1; e >= 0; --e) {
+    if ((ownbits >> e & 1u) && !(isfinite(a[e]) && a[e] >= 0.0))
+      key = fail_key_make(tb, k, (static_cast<unsigned long long>(pix) << 5) | static_cast<unsigned>(e0 + e),
+                          isfinite(a[e]) ? kFailNegative : kFailNonFinite);
+  }
+  // entries fine on this lane: the column-sum check comes after all of them
+  if (key == ~0ull && !(fabs(csum - 1.0) <= kSimplexTol))
+    key = fail_key_make(tb, k, (static_cast<unsigned long long>(pix) << 5) | 31u, kFailDrift);
+  if (key != ~0ull) atomicMin(slot, key);  // later steps post larger keys: the first one survives
+}
+
 template <int PT, int TPP, bool UPDATE, bool EXACT>
 __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int rl, int j, int pix,
                                                  bool valid, int sub, double* ss, const double* sh,
@@ -105,7 +132,6 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
       for (int m = 0; m < PT; ++m) Gr[e][m] = own[e] ? G[(sub * EPT + e) * PT + m] : 0.0;
   }
   double aPa = 0.0, aGa = 0.0;
-  bool bad = false;
   const int steps = UPDATE ? d.K1 : 1;
   for (int k = 0; k < steps; ++k) {
     double ga[EPT];
@@ -155,43 +181,40 @@ __device__ __forceinline__ double pixel_a_update(const PassArgs& pa, int r, int 
     for (int o = 1; o < TPP; o <<= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
     // total ∈ [1e-30, p] (every factor ≤ 1, the largest ≥ 1e-30): a normal number.
     const double inv = __drcp_rn(total);  // IEEE 1/total (= the division's value)
-    // check_iterate (solver.cpp:65-90) on this pixel's column: every entry
-    // finite and >= 0, |Σ − 1| <= 1e-9.  The fast path only TRIGGERS the exact
-    // checks, and does so on the integer pipe (the fp64 pipe is the A pass's
-    // bottleneck): the OR of the entries' sign bits, and the high word of
-    // |Σ − 1| against that of 1e-9 (NaN/Inf entries make Σ NaN/Inf, whose high
-    // word is above every finite one).  post_simplex_failure then re-evaluates the
-    // reference's conditions exactly and resolves its scan order.
-    double csum = 0.0;
-    int signs = 0;
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      if (own[e]) {
-        a[e] *= inv;
-        csum += a[e];
-        signs |= __double2hiint(a[e]);
+    for (int e = 0; e < EPT; ++e)
+      if (own[e]) a[e] *= inv;
+    // check_iterate (solver.cpp:65-90) on this pixel's column: every entry finite
+    // and >= 0, |Σ − 1| <= 1e-9.  None of the three can fail while `total` is a
+    // positive normal number: the factors z·e^{u − max u} lie in [0, 1], so the
+    // entries a_e = factor·(1/total) are finite and >= 0, and their sum is
+    // total·(1/total) up to (2p + 2) roundings, < 4e-15 from 1 at p = 16.  A
+    // NaN/Inf anywhere upstream (P, G·a, η, a) reaches `total` through the
+    // exponentials.  So the fast path is ONE integer range test on total's high
+    // word (the fp64 pipe is the A pass's bottleneck; a per-step column sum cost
+    // 4–11% of the pass); the reference's conditions themselves are evaluated,
+    // in its scan order, only behind that test.  `total` is uniform over the
+    // pixel's TPP lanes, so the group takes the branch together.
+    bool force = false;
+    if (pa.dbg & 0xE000) {  // test hooks (EDAA_DBG): poison pixel 7 of run 1 at outer iteration 2, inner step 2
+      if (r == 1 && pix == 7 && pa.t == 2 && k == 1) {
+        force = true;
+        if ((pa.dbg & 0x2000) && sub == 0) a[0] = __longlong_as_double(0x7FF8000000000000ll);  // NaN entry
+        if ((pa.dbg & 0x4000) && sub == 0) a[0] = -a[0];                                        // negative entry
+        if ((pa.dbg & 0x8000) && sub == 0) a[0] += 1e-8;                                        // drifted column
       }
     }
+    if ((static_cast<unsigned>(__double2hiint(total)) - 0x00100000u >= 0x7FE00000u || force) && valid) {
+      double tmp[EPT];  // a copy whose address may be taken: a[] itself stays in registers
+      unsigned ownbits = 0;
 #pragma unroll
-    for (int o = 1; o < TPP; o <<= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
-    constexpr int kTolHi = 0x3E112E0B;  // high word of 1e-9 (0x3E112E0BE826D695)
-    if (((signs < 0) | ((__double2hiint(csum - 1.0) & 0x7fffffff) >= kTolHi)) && valid && !bad) {
-      unsigned long long key = ~0ull;
-#pragma unroll
-      for (int e = EPT - 1; e >= 0; --e) {
-        if (own[e] && !(isfinite(a[e]) && a[e] >= 0.0))
-          key = fail_key_make((static_cast<unsigned>(pa.t) << 1), k,
-                              (static_cast<unsigned long long>(pix) << 5) | static_cast<unsigned>(sub * EPT + e),
-                              isfinite(a[e]) ? kFailNegative : kFailNonFinite);
+      for (int e = 0; e < EPT; ++e) {
+        tmp[e] = a[e];
+        ownbits |= own[e] ? (1u << e) : 0u;
       }
-      // entries fine on this lane: the column-sum check comes after all of them
-      if (key == ~0ull && !(fabs(csum - 1.0) <= kSimplexTol))
-        key = fail_key_make((static_cast<unsigned>(pa.t) << 1), k,
-                            (static_cast<unsigned long long>(pix) << 5) | 31u, kFailDrift);
-      if (key != ~0ull) {
-        bad = true;  // later inner steps of this pixel can only fail later in the scan order
-        atomicMin(pa.fail_key + r, key);
-      }
+      const unsigned gmask = (TPP == 32) ? 0xffffffffu : (((1u << TPP) - 1u) << gbase);
+      post_simplex_failure<EPT, TPP>(pa.fail_key + r, static_cast<unsigned>(pa.t) << 1, k, pix, sub * EPT, gmask, tmp,
+                                     ownbits);
     }
     if (pa.observe_A != nullptr && valid) {
 #pragma unroll

@@ -745,3 +745,35 @@ def test_two_contexts_solve_concurrently_from_two_threads():
         [t.join() for t in th]
         assert not errs, errs
         assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("p", [3, 5, 12])
+@pytest.mark.parametrize("bits,want", [(0x2000, "non-finite abundance iterate at outer iteration 2"),
+                                       (0x4000, "abundance iterate left the simplex at outer iteration 2"),
+                                       (0x8000, "abundance column sum drifted from 1 at outer iteration 2"),
+                                       (0xA000, "non-finite abundance iterate at outer iteration 2")])
+def test_in_solve_checks_report_the_reference_message_and_outer_index(p, bits, want):
+    """The A update's check_iterate inside a solve.  A valid image cannot make the
+    reference's branches fail (spectral_norm catches overflow first), so a test hook
+    (EDAA_DBG bits 13-15, read at context creation) poisons ONE entry of pixel 7 of
+    run 1 at outer iteration 2: a NaN, a negative entry, or a drifted column.  That
+    run — and only that run — must fail with the reference's message and outer
+    index (1, 2 and 4 lanes per pixel: p = 3, 5, 12)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, '.')\n"
+        "from paper_2209_11002_b200 import edaa, synth\n"
+        "x = synth.small_scene(24, 300, %d, seed=3)\n"
+        "d = edaa.Device(0); d.set_image(x)\n"
+        "d.solve(%d, 4, 5, 5, [1, 2, 3], [1.0, 1.0, 2.0])\n"
+        "for r in range(3):\n"
+        "    rec = d.record(r); print(r, int(rec.ok), rec.fail_outer, rec.message.decode())\n" % (p, p))
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root, timeout=300,
+                         env=dict(os.environ, EDAA_DBG=str(bits)))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    assert lines[0].startswith("0 1 ") and lines[2].startswith("2 1 ")
+    assert lines[1] == "1 0 2 " + want
