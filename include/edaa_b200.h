@@ -195,10 +195,11 @@ EDAA_API int edaa_set_shard_exchange(edaa_ctx* ctx, int mode);
 
 /* Order of the pass kernels' (pixel slice, run chunk) work items (no reference
  * counterpart: a scheduling knob of this implementation).  0 = auto (chunk-major
- * when X fits in L2, else slice-major), 1 = chunk-major, 2 = slice-major,
- * 3 = slice-major interleaved over the CTAs (CTA b takes items b, b+G, …, so
- * X slices are shared in L2: ~1/3 of the HBM traffic on images far larger
- * than L2, at about the same speed; plain slice-major if uneven).  The
+ * when X fits in L2, else slice-major interleaved over the CTAs when the items
+ * divide evenly), 1 = chunk-major, 2 = plain slice-major, 3 = slice-major
+ * interleaved (CTA b takes items b, b+G, …, so X slices are shared in L2: ~1/3
+ * of the HBM traffic on images far larger than L2, at about the same speed;
+ * plain slice-major if uneven).  The
  * per-(slice, chunk) partials, and so every result, are bitwise the same for
  * all orders; only the speed differs. */
 EDAA_API int edaa_set_pass_order(edaa_ctx* ctx, int order);
