@@ -201,8 +201,12 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
 #ifndef EDAA_KBR
 #define EDAA_KBR 8
 #endif
-constexpr int kBR = EDAA_KBR;  // band rows per CTA (a row's slice-sum order does not depend on it)
+constexpr int kBRMax = EDAA_KBR;  // band rows per CTA for full grids (a row's slice-sum order does not depend on it)
+// Small batches (few run chunks) launch the same kernel with fewer rows per CTA, so the
+// combine — latency-bound on NCH·⌈Lpad/kBR⌉ CTAs — still fills the GPU: at cfg0 (one
+// chunk) 8 rows per CTA is 20 CTAs and 15.7 µs per launch, as long as cfg1's 225.
 
+template <int kBR>
 __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
   griddep_launch_dependents();
   griddep_wait();
@@ -719,12 +723,19 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
     return cudaGetLastError();
   }
   if (a.mode != kModeA) {  // B step / init: normalisers, Y and Z in one kernel
+    // rows per CTA: the largest of 8, 4, 2, 1 that still gives at least one CTA per SM
+    int br = kBRMax;
+    while (br > 1 && d.NCH * ((d.Lpad + br - 1) / br) < d.ncta) br >>= 1;
+    const size_t smem = static_cast<size_t>(d.nslices) * kQMax * sizeof(double);
+    void (*kern)(CombineArgs) = br >= kBRMax ? k_combine_b<kBRMax> : br >= 8 ? k_combine_b<8> : br >= 4 ? k_combine_b<4>
+                                : br >= 2     ? k_combine_b<2>
+                                              : k_combine_b<1>;
+    const int rows = br >= kBRMax ? kBRMax : br >= 8 ? 8 : br >= 4 ? 4 : br >= 2 ? 2 : 1;
     // a constant, set on whichever device is current (per-device, per-function state)
-    const cudaError_t ea = cudaFuncSetAttribute(k_combine_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 kMaxSlices * kQMax * static_cast<int>(sizeof(double)));
     if (ea != cudaSuccess) return ea;
-    return launch_pdl(d.pdl != 0, k_combine_b, dim3(d.NCH, (d.Lpad + kBR - 1) / kBR), dim3(256),
-                      static_cast<size_t>(d.nslices) * kQMax * sizeof(double), st, a);
+    return launch_pdl(d.pdl != 0, kern, dim3(d.NCH, (d.Lpad + rows - 1) / rows), dim3(256), smem, st, a);
   }
   launch_pdl(d.pdl != 0, k_aat, dim3(d.NCH, (d.RC * d.p * d.p + 7) / 8 + 1), dim3(256), 0, st, a);
   cudaError_t e = cudaGetLastError();
