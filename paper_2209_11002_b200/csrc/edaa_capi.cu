@@ -387,7 +387,7 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   d.N = c->N;
   d.Npad = c->Npad;
   d.ntiles = d.Npad / edaa::kNP;
-  d.nslices = std::min(edaa::kMaxSlices, (d.ntiles + edaa::kTilesPerSlice - 1) / edaa::kTilesPerSlice);
+  d.nslices = edaa::slice_count(d.ntiles);
   d.sl0 = 0;
   d.sl1 = d.nslices;
   if (c->shard_world > 1) {

@@ -153,13 +153,15 @@ def run_ensemble_sharded(x, config: edaa.EnsembleConfig, group=None,
 
 NP = 32            # pixels per tile (csrc/edaa_internal.cuh kNP)
 TILES_PER_SLICE = 4
+SMALL_TILES_PER_SLICE = 2
 MAX_SLICES = 148
 
 
 def pixel_slices(pixels: int) -> int:
     """Number of pixel slices of an N-pixel image (a function of N only, as in make_dims)."""
     ntiles = -(-pixels // NP)
-    return min(MAX_SLICES, -(-ntiles // TILES_PER_SLICE))
+    tps = SMALL_TILES_PER_SLICE if ntiles <= 2 * MAX_SLICES else TILES_PER_SLICE   # edaa::slice_count
+    return min(MAX_SLICES, -(-ntiles // tps))
 
 
 def pixel_shard_plan(pixels: int, world: int, rank: int):
