@@ -238,11 +238,12 @@ EDAA_API int edaa_check_iterate(edaa_ctx* ctx, const double* m, size_t rows, siz
 /* Instrumentation.  With profiling on, every pass launch is bracketed by CUDA
  * events on edaa_stream(); edaa_profile_read returns, per pass kind, the
  * summed device time (ms) and launch count of the last finished solve
- * (kind 0 = init pass, 1 = A pass, 2 = B pass, 3 = objective pass).
+ * (kind 0 = init pass, 1 = A pass, 2 = B pass, 3 = objective pass, 4 = the
+ * combine kernels between the passes).
  * edaa_launch_count: kernels launched by this context since creation. */
 typedef struct {
-  double ms[4];
-  uint64_t launches[4];
+  double ms[5];
+  uint64_t launches[5];
 } edaa_profile;
 EDAA_API int edaa_profile_enable(edaa_ctx* ctx, int on);
 EDAA_API int edaa_profile_read(edaa_ctx* ctx, edaa_profile* out);

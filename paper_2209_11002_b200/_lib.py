@@ -37,7 +37,7 @@ class RunRecordC(C.Structure):
 
 
 class ProfileC(C.Structure):
-    _fields_ = [("ms", C.c_double * 4), ("launches", C.c_uint64 * 4)]
+    _fields_ = [("ms", C.c_double * 5), ("launches", C.c_uint64 * 5)]
 
 
 OBSERVER_FN = C.CFUNCTYPE(None, C.c_size_t, C.c_char, C.c_size_t, C.POINTER(C.c_double),

@@ -601,25 +601,36 @@ edaa::PostArgs post_args(edaa_ctx* c, int mode) {
   } while (0)
 #define EDAA_LAUNCH(ctx, call) EDAA_LAUNCH_N(ctx, call, 1)
 
+// Profiling brackets: an event pair of the given kind (0-3 = pass mode, 4 = combine) around
+// whatever is enqueued between prof_begin and prof_end.
+int prof_begin(edaa_ctx* c, int kind, cudaEvent_t* e1) {
+  *e1 = nullptr;
+  if (!c->profile) return EDAA_OK;
+  while (c->ev_pool.size() < 2 * (c->ev_used + 1)) {
+    cudaEvent_t e;
+    EDAA_CUDA(c, cudaEventCreate(&e));
+    c->ev_pool.push_back(e);
+  }
+  cudaEvent_t e0 = c->ev_pool[2 * c->ev_used];
+  *e1 = c->ev_pool[2 * c->ev_used + 1];
+  if (c->ev_kind.size() <= c->ev_used) c->ev_kind.resize(c->ev_used + 1);
+  c->ev_kind[c->ev_used] = kind;
+  ++c->ev_used;
+  EDAA_CUDA(c, cudaEventRecord(e0, c->stream));
+  return EDAA_OK;
+}
+int prof_end(edaa_ctx* c, cudaEvent_t e1) {
+  if (e1) EDAA_CUDA(c, cudaEventRecord(e1, c->stream));
+  return EDAA_OK;
+}
+
 // A pass launch, bracketed by events when profiling (kind = pass mode).
 int launch_pass_profiled(edaa_ctx* c, int mode, const edaa::PassArgs& pa) {
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (c->profile) {
-    while (c->ev_pool.size() < 2 * (c->ev_used + 1)) {
-      cudaEvent_t e;
-      EDAA_CUDA(c, cudaEventCreate(&e));
-      c->ev_pool.push_back(e);
-    }
-    e0 = c->ev_pool[2 * c->ev_used];
-    e1 = c->ev_pool[2 * c->ev_used + 1];
-    if (c->ev_kind.size() <= c->ev_used) c->ev_kind.resize(c->ev_used + 1);
-    c->ev_kind[c->ev_used] = mode;
-    ++c->ev_used;
-    EDAA_CUDA(c, cudaEventRecord(e0, c->stream));
-  }
+  cudaEvent_t e1 = nullptr;
+  int rc = prof_begin(c, mode, &e1);
+  if (rc) return rc;
   EDAA_LAUNCH(c, edaa::launch_pass(mode, pa, c->stream));
-  if (c->profile) EDAA_CUDA(c, cudaEventRecord(e1, c->stream));
-  return EDAA_OK;
+  return prof_end(c, e1);
 }
 
 // Observer hooks used by edaa_solve_observed (null in the batched path).
@@ -802,7 +813,15 @@ int run_pass(edaa_ctx* c, int mode, edaa::PassArgs pa) {
 // (cfg4 single run: 47.6 KB) instead of nslices·(L+24)·Q·8 (7 MB).  The sum
 // over ranks is NCCL's, so the sharded result equals the single-device one to
 // rounding (not bitwise; the broadcast exchange keeps the bitwise property).
+int combine_pass_impl(edaa_ctx* c, const edaa::CombineArgs& a, int nlaunch);
 int combine_pass(edaa_ctx* c, const edaa::CombineArgs& a, int nlaunch) {
+  cudaEvent_t e1 = nullptr;
+  int rc = prof_begin(c, 4, &e1);  // kind 4: the combine kernels (and, sharded, the exchange) of one pass
+  if (!rc) rc = combine_pass_impl(c, a, nlaunch);
+  if (!rc) rc = prof_end(c, e1);
+  return rc;
+}
+int combine_pass_impl(edaa_ctx* c, const edaa::CombineArgs& a, int nlaunch) {
   const Dims& d = c->d;
   const bool emul = c->shard_emulate > 1;
   if (c->shard_exchange != 0 || (!c->comm && !emul)) {

@@ -220,6 +220,37 @@ __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
   const int col0 = chunk * d.QCpad;
   const int S = d.nslices;
   const int ncol = min(d.RC, d.M - chunk * d.RC) * d.p;
+  // The row sums' operands first: every thread owns up to kIt (group, row, column) sums
+  // and issues the loads of its first kPre slices NOW, so their L2 latency overlaps the
+  // normaliser phase below (the products need e^{m_s − m}, the loads do not).  The
+  // accumulation order of a sum (slices ascending) is unchanged.
+  const int l0 = blockIdx.y * kBR;
+  const int nr = min(kBR, d.Lpad - l0);
+  const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
+  constexpr int kSums = kCG * kBR * kQMax;
+  constexpr int kIt = (kSums + 255) / 256;
+  constexpr int kPre = 4;
+  const double* src[kIt];
+  double v[kIt], pre[kIt][kPre];
+  int s0[kIt], len[kIt], xs[kIt], slot[kIt];
+  int maxlen = 0;
+#pragma unroll
+  for (int q = 0; q < kIt; ++q) {
+    const int e0 = tid + 256 * q;
+    const bool in = (kSums % 256 == 0) || e0 < kSums;
+    const int e = in ? e0 : 0;
+    const int x = e % kQMax, rest = e / kQMax;
+    const int rr = rest % kBR, g = rest / kBR;
+    s0[q] = (g * S) / kCG;
+    len[q] = (in && rr < nr) ? ((g + 1) * S) / kCG - s0[q] : 0;
+    src[q] = ca.part_C + static_cast<size_t>(l0 + min(rr, nr - 1)) * d.Qs + col0 + x;
+    xs[q] = x;
+    slot[q] = (g * kBR + rr) * kQMax + x;
+    v[q] = 0.0;
+    maxlen = max(maxlen, len[q]);
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) pre[q][k] = (k < len[q]) ? src[q][(s0[q] + k) * sstride] : 0.0;
+  }
   // Normalisers: 8 threads per column (192 threads for the 24 columns); thread t
   // of a column takes slices t, t+8, … with all its loads issued up front, then
   // an xor tree over the 8 (fixed order: a function of the slicing only).
@@ -283,35 +314,15 @@ __global__ void __launch_bounds__(256) k_combine_b(CombineArgs ca) {
     }
   }
   __syncthreads();
-  const int l0 = blockIdx.y * kBR;
-  const int nr = min(kBR, d.Lpad - l0);
-  const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
-  // kCG·kBR·kQMax = 768 (group, row, column) sums over 256 threads: each thread
-  // runs its three with interleaved loads (all of a group's slices in flight).
   {
-    constexpr int kSums = kCG * kBR * kQMax;
-    constexpr int kIt = (kSums + 255) / 256;
-    const double* src[kIt];
-    double v[kIt];
-    int s0[kIt], len[kIt], xs[kIt], slot[kIt];
-    int maxlen = 0;
 #pragma unroll
-    for (int q = 0; q < kIt; ++q) {
-      const int e0 = tid + 256 * q;
-      const bool in = (kSums % 256 == 0) || e0 < kSums;
-      const int e = in ? e0 : 0;
-      const int x = e % kQMax, rest = e / kQMax;
-      const int rr = rest % kBR, g = rest / kBR;
-      s0[q] = (g * S) / kCG;
-      len[q] = (in && rr < nr) ? ((g + 1) * S) / kCG - s0[q] : 0;
-      src[q] = ca.part_C + static_cast<size_t>(l0 + min(rr, nr - 1)) * d.Qs + col0 + x;
-      xs[q] = x;
-      slot[q] = (g * kBR + rr) * kQMax + x;
-      v[q] = 0.0;
-      maxlen = max(maxlen, len[q]);
+    for (int k = 0; k < kPre; ++k) {
+#pragma unroll
+      for (int q = 0; q < kIt; ++q)
+        if (k < len[q]) v[q] += pre[q][k] * facs[(s0[q] + k) * kQMax + xs[q]];
     }
 #pragma unroll 5
-    for (int k = 0; k < maxlen; ++k) {
+    for (int k = kPre; k < maxlen; ++k) {
 #pragma unroll
       for (int q = 0; q < kIt; ++q)
         if (k < len[q]) {

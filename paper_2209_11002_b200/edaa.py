@@ -398,10 +398,11 @@ class Device:
         self._check(self.lib.edaa_profile_enable(self.h, int(on)))
 
     def profile(self):
-        """Per pass kind (init, A, B, obj): (summed device ms, launches) of the last solve."""
+        """Per kind (the init / A / B / obj passes, and the combine kernels between them):
+        (summed device ms, launches) of the last solve."""
         pr = _lib.ProfileC()
         self._check(self.lib.edaa_profile_read(self.h, C.byref(pr)))
-        return {k: (pr.ms[i], int(pr.launches[i])) for i, k in enumerate(("init", "A", "B", "obj"))}
+        return {k: (pr.ms[i], int(pr.launches[i])) for i, k in enumerate(("init", "A", "B", "obj", "combine"))}
 
     def launch_count(self) -> int:
         return int(self.lib.edaa_launch_count(self.h))
