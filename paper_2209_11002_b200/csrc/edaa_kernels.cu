@@ -49,72 +49,17 @@ __device__ __forceinline__ void post_column_check(const CombineArgs& ca, int r, 
     atomicMin(ca.fail_key + r, fail_key_make(tb, ca.kin, col | ((1ull << 28) - 1), kFailDrift));
 }
 
-// the slices, fixed xor-tree merge (deterministic).
-__global__ void k_colnorm(CombineArgs ca) {
+// Final objective pass: trace[T] of every run = Σ over slices (ascending) of its objective terms.
+__global__ void k_rowsum(CombineArgs ca, int /*rows*/) {
   griddep_launch_dependents();
   griddep_wait();
   const Dims& d = ca.d;
-  const int col = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (col >= d.Qs) return;
   const int S = d.nslices;
-  double m = -INFINITY;
-  for (int sl = lane; sl < S; sl += 32) m = fmax(m, ca.part_m[static_cast<size_t>(sl) * d.Qs + col]);
-  m = warp_max(m);
-  double Ssum = 0.0;
-  for (int sl = lane; sl < S; sl += 32) {
-    const double ms = ca.part_m[static_cast<size_t>(sl) * d.Qs + col];
-    const double f = (ms == -INFINITY) ? 0.0 : exp(ms - m);
-    ca.fac[static_cast<size_t>(sl) * d.Qs + col] = f;
-    Ssum += ca.part_S[static_cast<size_t>(sl) * d.Qs + col] * f;
-  }
-  Ssum = warp_sum(Ssum);
-  // Mass of the normalised column b = e^{ℓ−m}/S, slice by slice (the drift check).
-  const double inv = 1.0 / Ssum;
-  double nsum = 0.0;
-  for (int sl = lane; sl < S; sl += 32)
-    nsum += ca.part_S[static_cast<size_t>(sl) * d.Qs + col] * ca.fac[static_cast<size_t>(sl) * d.Qs + col] * inv;
-  nsum = warp_sum(nsum);
-  if (lane != 0) return;
-  ca.colm[col] = m;
-  ca.colS[col] = Ssum;
-  ca.collogS[col] = log(Ssum);
-  const int chunk = col / d.QCpad, c = col % d.QCpad;
-  const int r = chunk * d.RC + c / d.p;
-  if (c < d.RC * d.p && r < d.M) post_column_check(ca, r, c % d.p, m, Ssum, nsum);
-}
-
-// Row sums over slices (fixed order): A mode → XAt / AAt; B/init → Y = Σ C_s·fac_s / S.
-// Block (32 columns × 8 rows); block (0,0) also folds the per-run objective.
-__global__ void k_rowsum(CombineArgs ca, int rows) {
-  griddep_launch_dependents();
-  griddep_wait();
-  const Dims& d = ca.d;
-  const int col = blockIdx.x * 32 + threadIdx.x;
-  const int row = blockIdx.y * 8 + threadIdx.y;
-  const int S = d.nslices;
-  if ((ca.mode == kModeA || ca.mode == kModeObj) && blockIdx.x == 0 && blockIdx.y == 0) {
-    for (int r = threadIdx.y * 32 + threadIdx.x; r < d.M; r += 256) {
-      double o = 0.0;
-      for (int sl = 0; sl < S; ++sl) o += ca.part_obj[static_cast<size_t>(sl) * d.M + r];
-      ca.trace[static_cast<size_t>(r) * ca.trace_stride + ca.trace_index] = o;
-    }
-  }
-  if (col >= d.Qs || row >= rows) return;
-  const double* src = ca.part_C + static_cast<size_t>(row) * d.Qs + col;
-  const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
-  double s = 0.0;
-  if (ca.mode == kModeA) {
-#pragma unroll 8
-    for (int sl = 0; sl < S; ++sl) s += src[sl * sstride];
-    if (row < d.Lpad)
-      ca.XAt[static_cast<size_t>(row) * d.Qs + col] = s;
-    else
-      ca.AAt[static_cast<size_t>(row - d.Lpad) * d.Qs + col] = s;
-  } else {
-#pragma unroll 8
-    for (int sl = 0; sl < S; ++sl) s += src[sl * sstride] * ca.fac[static_cast<size_t>(sl) * d.Qs + col];
-    ca.Y[static_cast<size_t>(row) * d.Qs + col] = s / ca.colS[col];
+  if (blockIdx.x != 0 || blockIdx.y != 0) return;
+  for (int r = threadIdx.y * 32 + threadIdx.x; r < d.M; r += 256) {
+    double o = 0.0;
+    for (int sl = 0; sl < S; ++sl) o += ca.part_obj[static_cast<size_t>(sl) * d.M + r];
+    ca.trace[static_cast<size_t>(r) * ca.trace_stride + ca.trace_index] = o;
   }
 }
 
@@ -127,11 +72,12 @@ __global__ void k_rowsum(CombineArgs ca, int rows) {
 // added in g order: one fixed order that depends on the slicing (a function of
 // N) only, so a run's arithmetic stays independent of its batch and position
 // (test_ensemble.cpp:150-169 analogue).
-//   B / init: Y rows = Σ_s C_s·e^{m_s−m} / S (fac, S from k_colnorm), then Z;
-//   A:        XAᵀ rows = Σ_s C_s, then Z with the block's Y and AAᵀ (k_aat).
+//   A:        XAᵀ rows = Σ_s C_s, then Z with the block's Y and AAᵀ (k_aat);
+//   B / init: Y rows = Σ_s C_s·e^{m_s−m} / S with the column normalisers, then Z.
 constexpr int kCR = 2;
 constexpr int kCG = 4;
 
+// A pass only (the B step / init combine is k_combine_b below, same summation order).
 __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
   griddep_launch_dependents();
   griddep_wait();
@@ -144,7 +90,6 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
   const int S = d.nslices;
   const int p = d.p;
   const int ncol = min(d.RC, d.M - static_cast<int>(blockIdx.x) * d.RC) * p;
-  const bool lse = (ca.mode == kModeB || ca.mode == kModeInit);
   const size_t sstride = static_cast<size_t>(d.Lrows) * d.Qs;
   const int l = blockIdx.y * kCR + rr;
   const bool live = (x < kQMax) && (l < d.Lpad);
@@ -152,14 +97,8 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
     const int s0 = (g * S) / kCG, s1 = ((g + 1) * S) / kCG;
     const double* src = ca.part_C + static_cast<size_t>(l) * d.Qs + col0 + x;
     double v = 0.0;
-    if (lse) {
-      const double* f = ca.fac + col0 + x;
 #pragma unroll 8
-      for (int sl = s0; sl < s1; ++sl) v += src[sl * sstride] * f[static_cast<size_t>(sl) * d.Qs];
-    } else {
-#pragma unroll 8
-      for (int sl = s0; sl < s1; ++sl) v += src[sl * sstride];
-    }
+    for (int sl = s0; sl < s1; ++sl) v += src[sl * sstride];
     red[y][x] = v;
   }
   __syncthreads();
@@ -167,15 +106,9 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
     double v = red[rr][x];
     for (int k = 1; k < kCG; ++k) v += red[k * kCR + rr][x];
     const size_t o = static_cast<size_t>(l) * d.Qs + col0 + x;
-    if (lse) {
-      v = (x < ncol) ? v / ca.colS[col0 + x] : 0.0;  // padding columns carry no run
-      ca.Y[o] = v;
-      ys[rr][x] = v;
-    } else {
-      ca.XAt[o] = v;
-      red[rr][x] = v;
-      ys[rr][x] = ca.Y[o];
-    }
+    ca.XAt[o] = v;
+    red[rr][x] = v;
+    ys[rr][x] = ca.Y[o];
   }
   if (ca.Z == nullptr) return;
   __syncthreads();
@@ -185,9 +118,7 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs ca) {
     const double* arow = ca.AAt + static_cast<size_t>(rl * p) * d.Qs + col0 + x;  // AAᵀ[rl·p+m][x]
     double sacc = 0.0;
     for (int mm = 0; mm < p; ++mm) sacc += ys[rr][rl * p + mm] * arow[static_cast<size_t>(mm) * d.Qs];
-    const size_t o = static_cast<size_t>(l) * d.Qs + col0 + x;
-    const double xa = lse ? ca.XAt[o] : red[rr][x];
-    ca.Z[o] = xa - sacc;
+    ca.Z[static_cast<size_t>(l) * d.Qs + col0 + x] = red[rr][x] - sacc;
   }
 }
 
@@ -729,7 +660,7 @@ cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st) {
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   const Dims& d = a.d;
   if (a.mode == kModeObj) {  // the final objective only
-    cudaError_t e0 = launch_pdl(d.pdl != 0, k_rowsum, dim3((d.Qs + 31) / 32, 1), dim3(32, 8), 0, st, a, 0);
+    cudaError_t e0 = launch_pdl(d.pdl != 0, k_rowsum, dim3(1, 1), dim3(32, 8), 0, st, a, 0);
     if (e0 != cudaSuccess) return e0;
     return cudaGetLastError();
   }
