@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                   "-I" + os.path.join(ROOT, "include")]
 CUDA_SRCS = (["edaa_pass_%s_%s.cu" % (x, m) for x in ("f32", "f64") for m in ("alo", "ahi", "b", "init", "obj")]
-             + ["edaa_kernels.cu", "edaa_prims.cu", "edaa_capi.cu"])
+             + ["edaa_pass_b64.cu", "edaa_kernels.cu", "edaa_prims.cu", "edaa_capi.cu"])
 HOST_SRCS = ["matrix.cpp", "image.cpp", "types.cpp", "solver.cpp", "ensemble.cpp", "device.cpp",
              # the formats and the front end either side of the path
              "npy.cpp", "envi.cpp", "metrics.cpp", "outputs.cpp", "synth.cpp", "cli.cpp"]

@@ -361,8 +361,8 @@ void shard_slices(const Dims& d, int rank, int world, int* sl0, int* sl1) {
 }
 // Pixel range of a slice range (tile-aligned; the last slice ends at Npad).
 void slice_pixels(const Dims& d, int sl0, int sl1, int* j0, int* j1) {
-  *j0 = static_cast<int>((static_cast<long long>(sl0) * d.ntiles) / d.nslices) * edaa::kNP;
-  *j1 = static_cast<int>((static_cast<long long>(sl1) * d.ntiles) / d.nslices) * edaa::kNP;
+  *j0 = edaa::slice_first_tile(d.ntiles, d.nslices, sl0) * edaa::kNP;
+  *j1 = edaa::slice_first_tile(d.ntiles, d.nslices, sl1) * edaa::kNP;
 }
 
 int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
@@ -429,6 +429,24 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   }
   if (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem))
     return set_err(c, EDAA_ERR_UNSUPPORTED, "tile working set exceeds shared memory");
+  // B pass with 64-pixel logical tiles (fp32 image) when its working set fits: 5 X slots, one W
+  // buffer, 3 or 2 state tiles.  A function of (L, p, image type) only.  EDAA_NO_B64=1 keeps k_pass.
+  d.npl = 1;
+  d.nbuf64 = d.nst64 = 0;
+  static const bool no_b64 = [] {
+    const char* v = std::getenv("EDAA_NO_B64");
+    return v && v[0] == '1';
+  }();
+  if (!no_b64 && d.xbytes == 4 && c->dbg == 0) {
+    for (int nst : {3, 2}) {
+      if (edaa::pass_b64_smem_bytes(d, 5, nst) <= static_cast<size_t>(edaa::kMaxSmem)) {
+        d.npl = 2;
+        d.nbuf64 = 5;
+        d.nst64 = nst;
+        break;
+      }
+    }
+  }
   *out = d;
   return EDAA_OK;
 }
@@ -1037,7 +1055,7 @@ static int prepare_image(edaa_ctx* c, size_t bands, size_t pixels, int xbytes) {
   EDAA_CUDA(c, cudaSetDevice(c->device));
   c->L = static_cast<int>(bands);
   c->N = static_cast<int>(pixels);
-  c->Npad = (c->N + edaa::kNP - 1) / edaa::kNP * edaa::kNP;
+  c->Npad = (c->N + edaa::kNPad - 1) / edaa::kNPad * edaa::kNPad;
   c->xbytes = xbytes;
   // A captured solve schedule reads X and ‖x‖² through their device addresses and
   // the shape through Dims (part of the graph key), so new contents in the same
@@ -1161,7 +1179,7 @@ static int ingest_impl(edaa_ctx* c, const T* x, size_t bands, size_t pixels, siz
   if (pixels > (1u << 30) || bands > (1u << 20)) return set_err(c, EDAA_ERR_UNSUPPORTED, "image too large");
   EDAA_CUDA(c, cudaSetDevice(c->device));
   const int L = static_cast<int>(bands), N = static_cast<int>(pixels);
-  const int Npad = (N + edaa::kNP - 1) / edaa::kNP * edaa::kNP;
+  const int Npad = (N + edaa::kNPad - 1) / edaa::kNPad * edaa::kNPad;
   const size_t raw_bytes = bands * pixels * sizeof(T), xn_bytes = static_cast<size_t>(L) * Npad * 8;
   EDAA_CUDA(c, ensure(c->in_raw, raw_bytes));
   EDAA_CUDA(c, ensure(c->in_x, xn_bytes));

@@ -28,7 +28,8 @@ namespace edaa {
 
 constexpr int kThreads = 512;   // 16 warps per CTA: 8 MMA warps + 8 update warps
 constexpr int kGroup = 256;     // threads per warp group
-constexpr int kNP = 32;         // pixels per tile
+constexpr int kNP = 32;         // pixels per tile (one X ring slot)
+constexpr int kNPad = 64;       // Npad granularity: an even number of tiles, so 64-pixel logical tiles never straddle a slice
 constexpr int kXST = kNP + 8;   // fp32 X tile row stride (conflict-free DMMA B-frags)
 constexpr int kSST = kNP + 4;   // fp64 weight tile row stride
 constexpr int kQMax = EDAA_QMAX;  // columns per chunk (kQMax/8 DMMA column tiles)
@@ -42,6 +43,10 @@ constexpr int kSmallTilesPerSlice = 2;  // images of at most 2·kMaxSlices tiles
 // passes fill more SMs and balance better: measured +9.5% on a single cfg0 run,
 // +2.5–13% on batches of 20–50 runs at N = 2,500–9,025; cfg1 (313 tiles) is
 // 10% slower with them (twice the slice partials), so larger images keep 4.
+// First 32-pixel tile of slice s: slices are made of 64-pixel tile PAIRS (ntiles is even).
+__host__ __device__ inline int slice_first_tile(int ntiles, int nslices, int s) {
+  return 2 * static_cast<int>((static_cast<long long>(s) * (ntiles / 2)) / nslices);
+}
 inline int slice_count(int ntiles) {
   const int tps = ntiles <= 2 * kMaxSlices ? kSmallTilesPerSlice : kTilesPerSlice;
   const int n = (ntiles + tps - 1) / tps;
@@ -98,6 +103,8 @@ struct Dims {
   int pdl;       // programmatic dependent launch for the schedule's kernels (small grids only)
   int cmajor;    // pass item order: 1 chunk-major (X fits in L2), 0 slice-major (edaa_pass.cuh)
   int ilv;       // slice-major items interleaved over the CTAs (A/B passes, separate instantiation)
+  int npl;       // B pass: 2 = the 64-pixel logical-tile kernel (edaa_pass_b64.cu), 1 = k_pass
+  int nbuf64, nst64;  // its X ring (32-pixel slots) and state-tile ring
 };
 
 struct PassArgs {
@@ -219,6 +226,8 @@ cudaError_t launch_shard_emul_sum(double* red, size_t stride, int world, size_t 
 cudaError_t launch_pack_cols(const double* src, double* stage, int rows, int Npad, int j0, int w, int wmax,
                              bool unpack, double* dst, cudaStream_t st);
 size_t pass_smem_bytes(const Dims& d, int nbuf);
+size_t pass_b64_smem_bytes(const Dims& d, int nbuf, int nst);
+cudaError_t launch_pass_b64(const PassArgs& a, cudaStream_t st);
 // primitives (edaa_prims.cu)
 cudaError_t launch_residual(const void* X, int xbytes, const double* Y, const double* A, double* R,
                             int L, int N, int Npad, int p, cudaStream_t st);

@@ -647,7 +647,9 @@ cudaError_t launch_pass(int mode, const PassArgs& a, cudaStream_t st) {
   const bool lo = a.d.p <= 5;
   switch (mode) {
     case kModeInit: return f64 ? launch_pass_f64_init(a, st) : launch_pass_f32_init(a, st);
-    case kModeB: return f64 ? launch_pass_f64_b(a, st) : launch_pass_f32_b(a, st);
+    case kModeB:
+      if (!f64 && a.d.npl == 2 && a.kprof == nullptr) return launch_pass_b64(a, st);
+      return f64 ? launch_pass_f64_b(a, st) : launch_pass_f32_b(a, st);
     case kModeObj: return f64 ? launch_pass_f64_obj(a, st) : launch_pass_f32_obj(a, st);
     case kModeA:
       if (f64) return lo ? launch_pass_f64_alo(a, st) : launch_pass_f64_ahi(a, st);

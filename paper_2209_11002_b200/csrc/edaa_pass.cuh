@@ -326,7 +326,7 @@ struct Cursor {
 };
 
 __host__ __device__ __forceinline__ int slice_tile(const Dims& d, int s) {
-  return (s * d.ntiles) / d.nslices;  // < 2^31: ntiles ≤ 2^25, nslices ≤ 296
+  return slice_first_tile(d.ntiles, d.nslices, s);  // tile pairs: every slice holds an even number of tiles
 }
 // slt: the CTA's shared-memory copy of slice_tile(d, 0 .. nslices) (no divisions per tile)
 // Item order (local index k over the owned slices [sl0, sl1)):

@@ -159,7 +159,7 @@ MAX_SLICES = 148
 
 def pixel_slices(pixels: int) -> int:
     """Number of pixel slices of an N-pixel image (a function of N only, as in make_dims)."""
-    ntiles = -(-pixels // NP)
+    ntiles = 2 * -(-pixels // (2 * NP))   # Npad is a multiple of 64: an even number of 32-pixel tiles
     tps = SMALL_TILES_PER_SLICE if ntiles <= 2 * MAX_SLICES else TILES_PER_SLICE   # edaa::slice_count
     return min(MAX_SLICES, -(-ntiles // tps))
 
@@ -167,12 +167,13 @@ def pixel_slices(pixels: int) -> int:
 def pixel_shard_plan(pixels: int, world: int, rank: int):
     """(first slice, end slice, first pixel, end pixel) owned by `rank` — the
     device's shard_slices / slice_pixels, clipped to the image."""
-    ntiles = -(-pixels // NP)
+    ntiles = 2 * -(-pixels // (2 * NP))
     ns = pixel_slices(pixels)
     if ns < world:
         raise edaa.EdaaError("image too small to shard its pixels over that many devices")
     s0, s1 = rank * ns // world, (rank + 1) * ns // world
-    j0, j1 = (s0 * ntiles // ns) * NP, (s1 * ntiles // ns) * NP
+    # edaa::slice_first_tile: slices are made of 64-pixel tile pairs
+    j0, j1 = 2 * (s0 * (ntiles // 2) // ns) * NP, 2 * (s1 * (ntiles // 2) // ns) * NP
     return s0, s1, min(j0, pixels), min(j1, pixels)
 
 
