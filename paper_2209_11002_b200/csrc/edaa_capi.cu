@@ -437,7 +437,7 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
     const char* v = std::getenv("EDAA_NO_B64");
     return v && v[0] == '1';
   }();
-  if (!no_b64 && d.xbytes == 4 && c->dbg == 0) {
+  if (!no_b64 && d.xbytes == 4 && (c->dbg & ~258) == 0) {  // it honours EDAA_DBG bits 2 and 256 only
     for (int nst : {3, 2}) {
       if (edaa::pass_b64_smem_bytes(d, 5, nst) <= static_cast<size_t>(edaa::kMaxSmem)) {
         d.npl = 2;

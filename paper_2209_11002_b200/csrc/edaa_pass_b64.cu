@@ -344,6 +344,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
       if (nst == 3) cp_async_wait2(); else cp_async_wait1();  // st(i) landed
       bar_sync(bars::kUpd, kGroup);
       mbar_wait(sready + (it & 1), (it >> 1) & 1);  // S(i) ready
+      if (pa.dbg & 256) {  // development (EDAA_DBG=256, as in k_pass): bare hand-shake, no update work
+        warp_arrive(wready + (it & 1));
+        cursor_next_t<ILV>(p2c, d, slt);
+        cursor_next_t<ILV>(p2c, d, slt);
+        stu = (stu + 1 == nst) ? 0 : stu + 1;
+        continue;
+      }
       double* ss = sbuf(it);
       const double* st = stslot(stu);
       stu = (stu + 1 == nst) ? 0 : stu + 1;
@@ -379,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
           mn = fmax(mo, tmax);
 #pragma unroll
           for (int k = 0; k < PPL; ++k) {
-            const double w = (mn == -INFINITY) ? 0.0 : exp_nonpos(ell[k] - mn, etab);
+            const double w = (pa.dbg & 2) ? 1.0 : ((mn == -INFINITY) ? 0.0 : exp_nonpos(ell[k] - mn, etab));
             ss[c * kSST2 + k * 8 + l8] = w;
             tsum += w;
           }
