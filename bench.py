@@ -448,7 +448,8 @@ def main():
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
         "frac": achieved / peak64 if peak64 else None, "traffic": traffic,
-        "kernel": "k_pass<B> (g = XᵀZ, logits, online max, Y = X·B; fp64 DMMA)",
+        "kernel": "B pass: k_pass_b64 (64-pixel logical tiles; fp32 images with L <= 200) or k_pass<B> "
+                  "(g = XᵀZ, logits, online max, Y = X·B; fp64 DMMA)",
         "peak_source": "fp64 DMMA microkernel measured live (edaa_probe_fp64_peak); "
                        "MEASURED_PEAKS.json has no fp64 entry",
         "flops_per_launch": flops_b, "launch_ms": launch_ms,

@@ -39,7 +39,9 @@ for name, c in per.items():
     d = dm.get(name, name)
     d = re.sub(r"\(edaa::PassArgs.*", "", d).replace("void edaa::", "").replace("pass_impl::", "").replace("(anonymous namespace)::", "")
     key = re.sub(r"\(.*", "", re.sub(r"<.*", "", d)).replace("void ", "").replace("edaa::", "")
-    if "k_pass" in d:
+    if "k_pass_b64" in d:
+        key = "k_pass_b64 (B pass, 64-pixel logical tiles)"
+    elif "k_pass" in d:
         m = re.search(r"k_pass<(?:\(int\))?(\d), (?:\(int\))?(\d+), (?:\(int\))?(\d), (\w+), ", d)
         mode = {"0": "init", "1": "A", "2": "B", "3": "obj"}[m.group(1)] if m else "?"
         key = "k_pass<%s, %s>" % (mode, m.group(4) if m else "?")
