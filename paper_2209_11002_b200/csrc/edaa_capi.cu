@@ -430,22 +430,17 @@ int make_dims(edaa_ctx* c, const edaa_solve_params* prm, Dims* out) {
   if (edaa::pass_smem_bytes(d, d.nbuf) > static_cast<size_t>(edaa::kMaxSmem))
     return set_err(c, EDAA_ERR_UNSUPPORTED, "tile working set exceeds shared memory");
   // B pass with 64-pixel logical tiles (fp32 image) when its working set fits: 5 X slots, one W
-  // buffer, 3 or 2 state tiles.  A function of (L, p, image type) only.  EDAA_NO_B64=1 keeps k_pass.
+  // buffer, the S tiles.  A function of (L, p, image type) only.  EDAA_NO_B64=1 keeps k_pass.
   d.npl = 1;
-  d.nbuf64 = d.nst64 = 0;
+  d.nbuf64 = 0;
   static const bool no_b64 = [] {
     const char* v = std::getenv("EDAA_NO_B64");
     return v && v[0] == '1';
   }();
-  if (!no_b64 && d.xbytes == 4 && (c->dbg & ~258) == 0) {  // it honours EDAA_DBG bits 2 and 256 only
-    for (int nst : {3, 2}) {
-      if (edaa::pass_b64_smem_bytes(d, 5, nst) <= static_cast<size_t>(edaa::kMaxSmem)) {
-        d.npl = 2;
-        d.nbuf64 = 5;
-        d.nst64 = nst;
-        break;
-      }
-    }
+  if (!no_b64 && d.xbytes == 4 && (c->dbg & ~258) == 0 &&  // it honours EDAA_DBG bits 2 and 256 only
+      edaa::pass_b64_smem_bytes(d, 5) <= static_cast<size_t>(edaa::kMaxSmem)) {
+    d.npl = 2;
+    d.nbuf64 = 5;
   }
   *out = d;
   return EDAA_OK;

@@ -104,7 +104,7 @@ struct Dims {
   int cmajor;    // pass item order: 1 chunk-major (X fits in L2), 0 slice-major (edaa_pass.cuh)
   int ilv;       // slice-major items interleaved over the CTAs (A/B passes, separate instantiation)
   int npl;       // B pass: 2 = the 64-pixel logical-tile kernel (edaa_pass_b64.cu), 1 = k_pass
-  int nbuf64, nst64;  // its X ring (32-pixel slots) and state-tile ring
+  int nbuf64;    // its X ring (32-pixel slots)
 };
 
 struct PassArgs {
@@ -226,7 +226,7 @@ cudaError_t launch_shard_emul_sum(double* red, size_t stride, int world, size_t 
 cudaError_t launch_pack_cols(const double* src, double* stage, int rows, int Npad, int j0, int w, int wmax,
                              bool unpack, double* dst, cudaStream_t st);
 size_t pass_smem_bytes(const Dims& d, int nbuf);
-size_t pass_b64_smem_bytes(const Dims& d, int nbuf, int nst);
+size_t pass_b64_smem_bytes(const Dims& d, int nbuf);
 cudaError_t launch_pass_b64(const PassArgs& a, cudaStream_t st);
 // primitives (edaa_prims.cu)
 cudaError_t launch_residual(const void* X, int xbytes, const double* Y, const double* A, double* R,

@@ -8,8 +8,9 @@
 // covers 64 pixels.  Shared memory (227 KB) then holds, at L = 198: 5 X slots of 32 pixels
 // (128 KB; P3 releases its first slot half-way so the ring stays one slot short of three
 // logical tiles), ONE W chunk buffer (41.6 KB), the S / w tiles without the band-half split
-// (P1 = 8 pixel groups × all bands: 2 × 13 KB) and 2–3 state tiles (12.3 KB each).  It fits
-// for L ≤ 200 with a 24-column chunk; other shapes (and fp64 images) keep k_pass.
+// (P1 = 8 pixel groups × all bands: 2 × 13 KB) and no state tiles (the logits come from global
+// memory into registers).  It fits for L ≤ 232 with a 24-column chunk (cfg0–cfg4); other shapes
+// and fp64 images keep k_pass.
 //
 // Partial sums: P3 accumulates the same 32-pixel k-step sequence per slice as k_pass (two
 // slots in order = two tiles in order) and flushes per (slice, chunk) item, so Y is bitwise
@@ -26,12 +27,13 @@ constexpr int kSST2 = kNP2 + 4;   // S / w tile row stride (doubles): ≡ 8 word
 constexpr int kMaxRing = 8;
 
 struct Lay64 {
-  int xs_off, xs_bytes, ws_off, ws_bytes, ss_off, buf_bytes, st_off, st_bytes, col_off, tab_off, slt_off, mbar_off,
-      total;
+  int xs_off, xs_bytes, ws_off, ws_bytes, ss_off, buf_bytes, col_off, tab_off, slt_off, mbar_off, total;
 };
 
-// nbuf X slots (32 pixels each), one W chunk, kNSB S/w tiles [QCpad][kSST2], nst state tiles [QCpad][64].
-__host__ __device__ inline Lay64 layout_b64(const Dims& d, int nbuf, int nst) {
+// nbuf X slots (32 pixels each), one W chunk, kNSB S/w tiles [QCpad][kSST2].  No state tiles: the
+// update reads its logits straight from global memory into registers ahead of the wait for S(i)
+// (measured equal to a cp.async state ring at cfg1 / cfg2, and it is what lets L = 224 fit).
+__host__ __device__ inline Lay64 layout_b64(const Dims& d, int nbuf) {
   Lay64 s;
   int off = 0;
   s.xs_off = off;
@@ -43,9 +45,6 @@ __host__ __device__ inline Lay64 layout_b64(const Dims& d, int nbuf, int nst) {
   s.buf_bytes = align16(d.QCpad * kSST2 * 8);
   s.ss_off = off;
   off += kNSB * s.buf_bytes;
-  s.st_bytes = align16(d.QCpad * kNP2 * 8);
-  s.st_off = off;
-  off += nst * s.st_bytes;
   s.col_off = off;  // m_run, S_run, c_m, c_eta (QCpad each), fac[2][QCpad]
   off += align16(6 * d.QCpad * 8);
   s.tab_off = off;
@@ -79,11 +78,11 @@ __device__ __forceinline__ void accumulate_slot(double (&ac)[RTW][kMaxCT][2], co
 
 template <int RTW, int CTF, bool ILV>
 __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __grid_constant__ CUtensorMap xmap,
-                                                          int nbuf, int nst) {
+                                                          int nbuf) {
   extern __shared__ __align__(16) unsigned char smem[];
   using XT = float;
   const Dims& d = pa.d;
-  const Lay64 lay = layout_b64(d, nbuf, nst);
+  const Lay64 lay = layout_b64(d, nbuf);
   double* ws = reinterpret_cast<double*>(smem + lay.ws_off);
   int* slt = reinterpret_cast<int*>(smem + lay.slt_off);
   double* m_run = reinterpret_cast<double*>(smem + lay.col_off);
@@ -94,7 +93,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
   double* etab = reinterpret_cast<double*>(smem + lay.tab_off);
   auto xslot = [&](int b) { return reinterpret_cast<XT*>(smem + lay.xs_off + b * lay.xs_bytes); };
   auto sbuf = [&](int i) { return reinterpret_cast<double*>(smem + lay.ss_off + (i & 1) * lay.buf_bytes); };
-  auto stslot = [&](int b) { return reinterpret_cast<double*>(smem + lay.st_off + b * lay.st_bytes); };
 
   const int tid = threadIdx.x;
   const bool mma_group = tid < kGroup;
@@ -300,34 +298,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
     }
   } else {
     // ========================== update group ==========================
-    Cursor sc, p2c;
-    cursor_set_t<ILV>(sc, d, slt, item_begin);
+    Cursor p2c;
     cursor_set_t<ILV>(p2c, d, slt, item_begin);
     int cchunk = -1;
-    int stl = 0, stu = 0;  // state-tile ring (nst slots): next load, current use
-    auto next_state = [&](int f) {  // one commit group per call (empty past the end)
-      if (f < nlt) {
-        const ChunkInfo cn = chunk_info(d, sc.chunk);
-        double* st = stslot(stl);
-        const int j0 = sc.tile * kNP;
-        for (int e = gtid; e < cn.ncol * (kNP2 / 2); e += kGroup) {
-          const int c = e / (kNP2 / 2), q = e % (kNP2 / 2);
-          cp_async16(st + c * kNP2 + q * 2, pa.Lg + static_cast<size_t>(cn.srow0 + c) * d.Npad + j0 + q * 2);
-        }
-        stl = (stl + 1 == nst) ? 0 : stl + 1;
-        cursor_next_t<ILV>(sc, d, slt);
-        cursor_next_t<ILV>(sc, d, slt);
-      }
-      cp_async_commit();
-    };
-    for (int f = 0; f < nst - 1; ++f) next_state(f);
     for (int it = 0; it < nlt; ++it) {
       const ChunkInfo ci = chunk_info(d, p2c.chunk);
       const int j0 = p2c.tile * kNP;
       const bool item_first = p2c.tile == p2c.tstart;
       const bool item_last = p2c.tile + 2 == p2c.tend;
-      bar_sync(bars::kUpd, kGroup);  // everyone is done with st(i−1) and the previous item's scalars
-      next_state(it + nst - 1);      // into st(i−1)'s slot
+      bar_sync(bars::kUpd, kGroup);  // everyone is done with the previous tile's and item's scalars
       if (ci.chunk != cchunk) {
         if (gtid < kQMax) {
           const int c = gtid;
@@ -341,24 +320,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
         m_run[gtid] = -INFINITY;
         S_run[gtid] = 0.0;
       }
-      if (nst == 3) cp_async_wait2(); else cp_async_wait1();  // st(i) landed
+      constexpr int PPL = kNP2 / 8;
+      const int uc = gtid >> 3, ul8 = gtid & 7;  // 8 lanes per column, 8 pixels per lane (j = k·8 + l8)
+      double lg[PPL];  // the lane's 8 logits, in flight across the barrier and the wait for S(i)
+#pragma unroll
+      for (int k = 0; k < PPL; ++k) {
+        const int pix = j0 + k * 8 + ul8;
+        lg[k] = (uc < ci.ncol && pix < d.N) ? pa.Lg[static_cast<size_t>(ci.srow0 + uc) * d.Npad + pix] : 0.0;
+      }
       bar_sync(bars::kUpd, kGroup);
       mbar_wait(sready + (it & 1), (it >> 1) & 1);  // S(i) ready
       if (pa.dbg & 256) {  // development (EDAA_DBG=256, as in k_pass): bare hand-shake, no update work
         warp_arrive(wready + (it & 1));
         cursor_next_t<ILV>(p2c, d, slt);
         cursor_next_t<ILV>(p2c, d, slt);
-        stu = (stu + 1 == nst) ? 0 : stu + 1;
         continue;
       }
       double* ss = sbuf(it);
-      const double* st = stslot(stu);
-      stu = (stu + 1 == nst) ? 0 : stu + 1;
       double* fac = facb + (it & 1) * kQMax;
       {
-        // new logits; 8 lanes per column, 8 pixels per lane (j = k·8 + l8)
-        constexpr int PPL = kNP2 / 8;
-        const int c = gtid >> 3, l8 = gtid & 7;
+        // new logits
+        const int c = uc, l8 = ul8;
         const bool active = c < kQMax;
         double ell[PPL];
         double tmax = -INFINITY;
@@ -369,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
             const int j = k * 8 + l8, pix = j0 + j;
             double v = -INFINITY;
             if (real && pix < d.N) {
-              double lb = st[c * kNP2 + j] - c_m[c];                 // log b_old
+              double lb = lg[k] - c_m[c];                           // log b_old
               lb = (lb < log_floor()) ? log_floor() : lb;           // log max(b, 1e-30)
               v = lb + ss[c * kSST2 + j] * c_eta[c];                // + η_b·(−∇_B)
               pa.Lg[static_cast<size_t>(ci.srow0 + c) * d.Npad + pix] = v;
@@ -417,19 +399,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
 template <int RTW, int CTF>
 cudaError_t launch_b64_ctf(const PassArgs& a, cudaStream_t st) {
   const dim3 grid(std::min(a.d.NCH * (a.d.sl1 - a.d.sl0), a.d.ncta));
-  const size_t smem = layout_b64(a.d, a.d.nbuf64, a.d.nst64).total;
-  void (*kern)(PassArgs, CUtensorMap, int, int) = a.d.ilv ? k_pass_b64<RTW, CTF, true> : k_pass_b64<RTW, CTF, false>;
+  const size_t smem = layout_b64(a.d, a.d.nbuf64).total;
+  void (*kern)(PassArgs, CUtensorMap, int) = a.d.ilv ? k_pass_b64<RTW, CTF, true> : k_pass_b64<RTW, CTF, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   if (e != cudaSuccess) return e;
   e = launch_pdl(a.d.pdl != 0, kern, grid, dim3(kThreads), smem, st, a, *static_cast<const CUtensorMap*>(a.xmap),
-                 a.d.nbuf64, a.d.nst64);
+                 a.d.nbuf64);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 }  // namespace pass_impl
 
-size_t pass_b64_smem_bytes(const Dims& d, int nbuf, int nst) { return pass_impl::layout_b64(d, nbuf, nst).total; }
+size_t pass_b64_smem_bytes(const Dims& d, int nbuf) { return pass_impl::layout_b64(d, nbuf).total; }
 
 cudaError_t launch_pass_b64(const PassArgs& a, cudaStream_t st) {
   const bool wide = (a.d.Lpad / 8 + kQMax / 8) > 32;  // k_pass's RTW rule
