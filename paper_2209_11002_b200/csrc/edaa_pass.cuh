@@ -515,7 +515,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
   auto w_arrive = [&](int i) { warp_arrive(wready + (i & 1)); };
   auto w_wait = [&](int i) { mbar_wait(wready + (i & 1), (i >> 1) & 1); };
   if (tid < kQMax) facb[tid] = facb[kQMax + tid] = 1.0;
-  load_exp_table(etab, tid);
   griddep_launch_dependents();
   griddep_wait();  // the previous kernel's W / partial normalisers / state are complete
   __syncthreads();
@@ -769,6 +768,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass(PassArgs pa, const __grid_
     }
   } else {
     // ========================== update group ==========================
+    // the exp table is this group's alone: loaded here, off the MMA group's path to its first
+    // tile (the bar_sync at the top of the tile loop orders it before the first exp)
+    if (gtid < kExpTab) etab[gtid] = kExp2Tab[gtid];
     Cursor sc, p2c;
     cursor_set_t<ILV>(sc, d, slt, item_begin);
     cursor_set_t<ILV>(p2c, d, slt, item_begin);

@@ -137,7 +137,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
     if (lane == 0) mbar_arrive(bar);
   };
   if (tid < kQMax) facb[tid] = facb[kQMax + tid] = 1.0;
-  load_exp_table(etab, tid);
   griddep_launch_dependents();
   griddep_wait();
   __syncthreads();
@@ -298,6 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b64(PassArgs pa, const __g
     }
   } else {
     // ========================== update group ==========================
+    // the exp table is this group's alone: loaded here, off the MMA group's path to its first tile
+    // (the bar_sync at the top of the loop orders it before the first exp)
+    if (gtid < kExpTab) etab[gtid] = kExp2Tab[gtid];
     Cursor p2c;
     cursor_set_t<ILV>(p2c, d, slt, item_begin);
     int cchunk = -1;
