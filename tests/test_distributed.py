@@ -177,3 +177,20 @@ def test_pixel_shard_join_shares_one_communicator_id(tmp_path):
     assert (int(r0["rank"]), int(r1["rank"])) == (0, 1)
     assert int(r0["world"]) == int(r1["world"]) == 2 == int(r0["w"])
     assert r0["plan"][3] == r1["plan"][2] and r0["plan"][2] == 0 and r1["plan"][3] == 10000
+
+
+@pytest.mark.parametrize("pixels", [1, 63, 64, 65, 9025, 9472, 9473, 10000, 94249, 1048576])
+def test_pixel_slices_are_made_of_64_pixel_tile_pairs(pixels):
+    """edaa::slice_count / slice_first_tile (mirrored here): slice boundaries are multiples of 64
+    pixels — the B pass's 64-pixel logical tiles never straddle a slice — no slice is empty, and
+    small images (at most 296 tiles) take one tile pair per slice."""
+    ns = distributed.pixel_slices(pixels)
+    ntiles = 2 * -(-pixels // 64)
+    assert 1 <= ns <= distributed.MAX_SLICES
+    bounds = [2 * (s * (ntiles // 2) // ns) for s in range(ns + 1)]
+    assert bounds[0] == 0 and bounds[-1] == ntiles
+    assert all(b > a and (b - a) % 2 == 0 for a, b in zip(bounds, bounds[1:]))
+    if ntiles <= 2 * distributed.MAX_SLICES:
+        assert ns == ntiles // 2
+    # the plan of a 1-rank world covers the image
+    assert distributed.pixel_shard_plan(pixels, 1, 0) == (0, ns, 0, pixels)
